@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""TPLA decode-step benchmark (BASELINE.json metric: decode tokens/s & µs/layer at 32K ctx, DSV3 shape).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c3] [--impl tpla|reference]
+    torchrun --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A step = one pass of the whole hot path for one batch:
+K1 append of the new token's latent row (every sequence), then K2 absorb, K3 split-K attention,
+K4 combine, K5 W^UV + W^O up-projection and C1 all-reduce, on every one of the k TPLA ranks.
+
+Workload (default c1 = BASELINE configs[1]): DeepSeek-V3 attention layer, 128 heads, latent
+512 + RoPE 64, 32K cached tokens per sequence, batch 32, TPLA g = 2 on k = max(2, N) ranks.
+The total work is fixed, so scaling over N is "strong": N=1 runs both g=2 ranks on one GPU
+(they accumulate into y, standing in for the all-reduce), N=2 is the paper's TP=2 deployment
+(P:499), N=4/8 further split the heads inside each latent group.  Every N
+produces the same numbers.  The per-step cache (1.34 GB at N=1) exceeds L2 (126 MB), so
+every read comes from HBM without an explicit flush.
+
+Prints one JSON line (rank 0).  --impl reference times the fp64 oracle (oracle/) on the
+host cores instead: the one other place this file runs oracle code besides cpu_baseline.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "decode tokens/s & µs/layer at 32K ctx (DSV3 shape); HBM GB/s vs peak @1/2/4/8"
+
+WORKLOADS = {
+    "c1": dict(desc="configs[1]: DeepSeek-V3 attention layer decode, 128 heads, latent 512 + RoPE 64, "
+                    "32K context, batch 32, TPLA g=2", model="dsv3", B=32, S=32768, g=2, xform="hadamard"),
+    "c2": dict(desc="configs[2]: Kimi-K2 attention layer decode, 64 heads, latent 512 + RoPE 64, 32K context, "
+                    "batch 64, TPLA g=4", model="kimi", B=64, S=32768, g=4, xform="hadamard"),
+    "c3": dict(desc="configs[3]: DeepSeek-V3 decode at 128K context, batch 16, g=8, Hadamard-rotated cache",
+               model="dsv3", B=16, S=131072, g=8, xform="hadamard"),
+}
+SEED = 1001   # seed = 1000 + config index
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--workload", default="c1", choices=sorted(WORKLOADS))
+    p.add_argument("--impl", default="tpla", choices=["tpla", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
+    return p.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), float(pk["bf16_tflops"]), float(pk.get("bf16_tflops_sustained", 0)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ----------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML SM clock / throttle-reason sampler running during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], 0
+        self.ok = False
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples), "reasons": names}
+
+
+# ----------------------------------------------------------------------------------- CPU oracle leg
+def oracle_sample_timer(wl, k, g):
+    """Builds the fp64 oracle's inputs for ONE sequence of the workload and returns
+    run(h_s) -> seconds for one decode of that sequence restricted to h_s heads on every one of
+    the k ranks (all of the decode's per-sequence work scales linearly with the head count)."""
+    from oracle import numerics, plan as oplan, reparam, tpla
+    dims = synth.PRESETS[wl["model"]]
+    f64 = numerics.bf16_to_f64
+    S = wl["S"]
+    w = synth.gen_weights(dims, SEED)
+    U = reparam.hadamard_U(dims.d_c, SEED)
+    alpha = reparam.uniform_alpha(g)
+    c_raw = f64(synth.gen_raw_ckv(dims, S, SEED, 0))
+    k_pe = f64(synth.gen_kpe(dims, S, SEED, 0))
+    q, qpe = synth.gen_queries(dims, 1, SEED)
+    q, qpe = f64(q), f64(qpe)
+    per_group = k // g
+    plans_full = [oplan.make_plan(k, g, dims.h_q, dims.d_c, dims.d_r, r) for r in range(k)]
+    rows = {}
+    for pl in plans_full:
+        if pl.shard not in rows:
+            rows[pl.shard] = tpla.cache_rows(c_raw, k_pe, U, pl, alpha[pl.shard], 1e-6, tpla.EXACT)
+    W_UK, W_UV, gam = f64(w.W_UK), f64(w.W_UV), f64(w.gamma)
+    sm = 1.0 / math.sqrt(dims.d_h + dims.d_r)
+    h_loc = dims.h_q // per_group
+
+    W_UK_new, W_UV_new = tpla.reparam_weights(W_UK, W_UV, gam, U)      # offline conversion (a1, untimed)
+    eye = np.eye(dims.d_c)
+    cache = {}
+
+    def run(h_s: int) -> float:
+        """Seconds for the oracle's decode (Q' absorb, attention, W^UV, W^O) of one sequence
+        restricted to heads [head_begin, head_begin + h_s) of every rank."""
+        h_s = max(1, min(h_s, h_loc))
+        t = 0.0
+        for pl in plans_full:
+            sub = oplan.DevicePlan(pl.rank, pl.shard, pl.head_block, pl.head_begin, pl.head_begin + h_s,
+                                   pl.lat_begin, pl.lat_end, pl.row_width)
+            key = (pl.rank, h_s)
+            if key not in cache:
+                for old in [x for x in cache if x[1] != h_s]:
+                    del cache[old]
+                # gamma and U already absorbed above: convert with gamma = 1, U = I (pure slicing)
+                sub0 = oplan.DevicePlan(pl.rank, pl.shard, pl.head_block, 0, h_s, pl.lat_begin, pl.lat_end,
+                                        pl.row_width)
+                cols = slice(sub.head_begin * dims.d_h, sub.head_end * dims.d_h)
+                cache[key] = tpla.convert_weights(W_UK_new[:, cols], W_UV_new[:, cols], np.ones(dims.d_c),
+                                                  f64(w.W_O[cols]), eye, sub0, alpha[pl.shard], d_h=dims.d_h)
+            dw = cache[key]
+            t0 = time.perf_counter()
+            tpla.decode_device(q, qpe, [rows[pl.shard]], dw, sub, sm_scale=sm)
+            t += time.perf_counter() - t0
+        return t
+
+    return run, h_loc
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        n = max((i.get("num_threads", 1) for i in info), default=1)
+    except Exception:
+        n = None
+    return n or len(os.sched_getaffinity(0))
+
+
+def cpu_baseline(wl, k, g, budget_s: float):
+    run, h_loc = oracle_sample_timer(wl, k, g)
+    t1 = run(2)                                   # calibration (also warms BLAS)
+    per_head = max(t1 / 2, 1e-4)
+    h_s = int(max(1, min(h_loc, budget_s / 3 / per_head)))
+    reps, total, heads_done = 0, 0.0, 0
+    while total < budget_s and reps < 50:
+        total += run(h_s)
+        heads_done += h_s
+        reps += 1
+    sec_per_token = total / heads_done * h_loc     # one sequence, all heads, all k ranks
+    return {"value": 1.0 / sec_per_token, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+            "sample": (f"fp64 oracle decode of 1 sequence x {h_s} of {h_loc} heads on each of the k={k} ranks at "
+                       f"{wl['S']} context (weights absorbed per call), repeated {reps}x in {total:.1f}s; "
+                       f"tokens/s = heads_done / (time x {h_loc})"),
+            "us_per_layer": sec_per_token * wl["B"] * 1e6,
+            "host": {"affinity_cores": len(os.sched_getaffinity(0)), "cpu": _cpu_name()}}
+
+
+def _cpu_name():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def config_of(wl, N, k, g):
+    return {"workload": wl["desc"], "global_batch": wl["B"], "seq_len": wl["S"], "heads": synth.PRESETS[wl["model"]].h_q,
+            "latent": 512, "rope": 64, "g": g, "k": k, "ranks_per_gpu": k // N, "transform": wl["xform"],
+            "parallelism": f"tpla k={k} g={g} over {N} GPU(s)",
+            "l2": "no flush: per-step cache reads (>=0.5 GB) exceed the 126 MB L2",
+            "data": "synthetic (seeded bf16; DESIGN.md input recipe)"}
+
+
+def run_reference(args):
+    wl = WORKLOADS[args.workload]
+    N = args.gpus
+    k = max(N, wl["g"])
+    g = wl["g"]
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    budget = max(0.05, min(3.0, 150.0 / max(1, args.steps + args.warmup)))
+    run, h_loc = oracle_sample_timer(wl, k, g)
+    t1 = run(2)
+    h_s = int(max(1, min(h_loc, budget / max(t1 / 2, 1e-4))))
+    for _ in range(args.warmup):
+        run(h_s)
+    total = 0.0
+    for _ in range(args.steps):
+        total += run(h_s)
+    sec_per_token = total / (args.steps * h_s) * h_loc
+    value = 1.0 / sec_per_token
+    sample = (f"each step: fp64 oracle decode of 1 sequence x {h_s} of {h_loc} heads on each of the k={k} ranks at "
+              f"{wl['S']} context; tokens/s = heads / (time x {h_loc})")
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sec_per_token * wl["B"] * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": config_of(wl, N, k, g),
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------- GPU leg
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2508_15881_b200 import abi
+    from paper_2508_15881_b200.runtime import LayerSpec, TplaRank, bf16_from_bits
+
+    wl = WORKLOADS[args.workload]
+    N = args.gpus
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    proc = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == N, f"--gpus {N} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if N > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dims = synth.PRESETS[wl["model"]]
+    g = wl["g"]
+    k = max(N, g)
+    if k % N or dims.h_q % (k // g):
+        raise SystemExit(f"k={k} ranks cannot be spread over {N} GPUs")
+    m = k // N
+    my_ranks = list(range(proc * m, (proc + 1) * m))
+    B, S = wl["B"], wl["S"]
+    spec = LayerSpec(dims.h_q, dims.d_c, dims.d_r, dims.d_h, dims.D)
+
+    # ---- setup (untimed): weights, converted per rank; cache prefilled through K1 (EXACT rows)
+    w = synth.gen_weights(dims, SEED)
+    ranks = []
+    for r in my_ranks:
+        rk = TplaRank(spec, k=k, g=g, rank=r, batch=B, max_seq_len=S, device=dev)
+        rk.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_HADAMARD, sign_seed=SEED)
+        ranks.append(rk)
+    del w
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(SEED)
+    sig = torch.tensor(synth.latent_spectrum(dims.d_c, dims.n_outlier), dtype=torch.float32, device=dev)
+    pos_all = torch.arange(S - 1, dtype=torch.int32, device=dev)
+    for b in range(B):
+        ck = (torch.randn((S - 1, dims.d_c), generator=gen, device=dev) * sig).to(torch.bfloat16)
+        kp = torch.randn((S - 1, dims.d_r), generator=gen, device=dev).to(torch.bfloat16)
+        sq = torch.full((S - 1,), b, dtype=torch.int32, device=dev)
+        for rk in ranks:
+            rk.prefill(ck, kp, sq, pos_all)
+    del ck, kp, sq, pos_all
+    # per-step inputs: new latent row + RoPE key of every sequence at position S-1, queries
+    NP = 4
+    new_ck = [(torch.randn((B, dims.d_c), generator=gen, device=dev) * sig).to(torch.bfloat16) for _ in range(NP)]
+    new_kp = [torch.randn((B, dims.d_r), generator=gen, device=dev).to(torch.bfloat16) for _ in range(NP)]
+    qn = [torch.randn((B, dims.h_q, dims.d_h), generator=gen, device=dev).to(torch.bfloat16) for _ in range(NP)]
+    qp = [torch.randn((B, dims.h_q, dims.d_r), generator=gen, device=dev).to(torch.bfloat16) for _ in range(NP)]
+    seq_idx = torch.arange(B, dtype=torch.int32, device=dev)
+    pos_new = torch.full((B,), S - 1, dtype=torch.int32, device=dev)
+    seq_lens = torch.full((B,), S, dtype=torch.int32, device=dev)
+    y = torch.zeros((B, dims.D), dtype=torch.float32, device=dev)
+    out = torch.empty((B, dims.D), dtype=torch.bfloat16, device=dev)
+    comm = None
+    if N > 1:
+        obj = [abi.tpla_comm_unique_id() if proc == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = abi.tpla_comm_init(obj[0], N, proc)
+    stream = torch.cuda.current_stream()
+
+    def step(i, ck=None, kp=None, q=None, qq=None):
+        ck = new_ck[i % NP] if ck is None else ck
+        kp = new_kp[i % NP] if kp is None else kp
+        q = qn[i % NP] if q is None else q
+        qq = qp[i % NP] if qq is None else qq
+        for rk in ranks:
+            rk.append(ck, kp, seq_idx, pos_new, abi.RMS_SLICED)
+        for j, rk in enumerate(ranks):
+            last = j == len(ranks) - 1
+            rk.decode(q, qq, seq_lens, y, out if last else None, accumulate=j > 0, comm=comm if last else None)
+
+    def barrier():
+        if N > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if N == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(args.warmup):
+        step(i)
+    abi.tpla_sync(stream.cuda_stream)
+
+    # ---- timed region (device-timed with CUDA events on the launching stream)
+    abi.tpla_profile_reset()
+    abi.tpla_profile_enable(True)
+    barrier()
+    torch.cuda.synchronize()
+    n0 = abi.tpla_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = abi.tpla_launch_count() - n0
+    abi.tpla_profile_enable(False)
+    prof = abi.profile_table()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_step = ms / args.steps
+    value = B * args.steps / (ms / 1e3)
+    abi.tpla_sync(stream.cuda_stream)
+
+    # ---- roofline of the dominant kernel (K3 attention), per launch = one rank's shard
+    hbm, tf_burst, tf_sust, peak_src = load_peaks()
+    k3_name = next((n for n in prof if n.startswith("K3")), None)
+    plan0 = ranks[0].plan
+    bytes_k3 = B * S * plan0.row_width * 2                       # Σ_b S_b · W · 2
+    flops_k3 = 2 * B * S * plan0.h_loc * (2 * plan0.w_lat + dims.d_r)
+    k3_ms, k3_n = prof.get(k3_name, (float("nan"), 1))
+    k3_avg_s = k3_ms / max(k3_n, 1) / 1e3
+    gbs = bytes_k3 / k3_avg_s / 1e9
+    tfs = flops_k3 / k3_avg_s / 1e12
+    bound = "hbm" if bytes_k3 / (hbm * 1e9) >= flops_k3 / (tf_burst * 1e12) else "tensor"
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        if k3_name in tr and tr[k3_name].get("workload") == args.workload:
+            traffic = tr[k3_name]["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    step_gpu_ms = sum(v[0] for v in prof.values()) / args.steps
+    roofline = {"bound": bound, "achieved": gbs if bound == "hbm" else tfs, "peak": hbm if bound == "hbm" else tf_burst,
+                "unit": "GB/s" if bound == "hbm" else "TFLOP/s", "frac": (gbs / hbm) if bound == "hbm" else (tfs / tf_burst),
+                "traffic": traffic, "kernel": k3_name, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": bytes_k3, "algorithmic_flops_per_launch": flops_k3,
+                "avg_launch_us": k3_avg_s * 1e6, "launches": k3_n,
+                "tensor_tflops": tfs, "tensor_frac_of_burst": tfs / tf_burst,
+                "share_of_step": (k3_ms / args.steps) / step_gpu_ms if step_gpu_ms > 0 else None}
+    kernels = {n: {"us_per_step": v[0] / args.steps * 1e3, "launches_per_step": v[1] / args.steps}
+               for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside the region
+    e2e = None
+    if not args.no_e2e:
+        h_ck = [x.cpu().pin_memory() for x in new_ck]
+        h_kp = [x.cpu().pin_memory() for x in new_kp]
+        h_q = [x.cpu().pin_memory() for x in qn]
+        h_qp = [x.cpu().pin_memory() for x in qp]
+        h_out = torch.empty((B, dims.D), dtype=torch.bfloat16).pin_memory()
+        d_ck, d_kp = torch.empty_like(new_ck[0]), torch.empty_like(new_kp[0])
+        d_q, d_qp = torch.empty_like(qn[0]), torch.empty_like(qp[0])
+        h2d = sum(t.numel() * t.element_size() for t in (h_ck[0], h_kp[0], h_q[0], h_qp[0]))
+        d2h = h_out.numel() * h_out.element_size()
+        n_e2e = max(10, min(args.steps, 100))
+        for i in range(3):
+            step(i)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(n_e2e):
+            j = i % NP
+            d_ck.copy_(h_ck[j], non_blocking=True)
+            d_kp.copy_(h_kp[j], non_blocking=True)
+            d_q.copy_(h_q[j], non_blocking=True)
+            d_qp.copy_(h_qp[j], non_blocking=True)
+            step(i, d_ck, d_kp, d_q, d_qp)
+            h_out.copy_(out, non_blocking=True)
+            stream.synchronize()          # the host consumes each step's output before the next
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": B * n_e2e / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": n_e2e, "ms_per_step": ems / n_e2e}
+
+    cpu = None
+    if proc == 0 and N == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, k, g, args.cpu_seconds)
+
+    if comm is not None:
+        abi.tpla_comm_destroy(comm)
+    if proc == 0:
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "us_per_layer": ms_step * 1e3,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic", "impl": "tpla", "config": config_of(wl, N, k, g),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "gpu_launches_per_step": launches / args.steps, "clocks": clocks.summary(), "kernels": kernels,
+                "hbm_gbs_per_gpu_k3": gbs, "kv_bytes_per_gpu_per_step": bytes_k3 * len(ranks)}
+        print(json.dumps(line), flush=True)
+    if N > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,236 @@
+/*
+ * tpla.h — C ABI of libtpla.so, the B200 (sm_100a) decode hot path of
+ * Tensor-Parallel Latent Attention (TPLA, arXiv 2508.15881).
+ *
+ * Citations: "P:n" = line n of the paper text, with its section.
+ *
+ * The path, per layer, per decode step, on each device (rank r of k):
+ *   tpla_append_kv   K1  transform + (sliced) RMSNorm + slice + bf16 store  §4.1/§4.3
+ *   tpla_decode      K2  Q'_j = q W^UK'_j^T (mu_j folded)                     §3.3/§4.2
+ *                    K3  per-shard split-K flash decoding over [ĉ_j ‖ k^PE]  §4, Eq. tpla_softmax_one_device
+ *                    K4  split-K combine
+ *                    K5  Õ_j = O_j W^UV'_j W^O_rows                           §4; W^VO factored P:114
+ *                    C1  O = AllReduce(Σ Õ_j)  (NCCL, sum, fp32)              §4
+ *
+ * Conventions (all entry points):
+ *  - Every tensor argument is a plain pointer.  "device" pointers are CUDA
+ *    device memory owned by the caller (the Python side allocates them with
+ *    PyTorch); "host" pointers are ordinary host memory.  The library never
+ *    allocates device memory on the decode path: scratch comes from the caller's
+ *    workspace, sized by tpla_decode_workspace_bytes().  The only object the
+ *    library owns is tpla_comm (an NCCL communicator).
+ *  - bf16 tensors are passed as their 16-bit patterns (uint16).  Row-major,
+ *    densely packed, 16-byte aligned base addresses, unless stated otherwise.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    All device work is asynchronous on that stream, NCCL included, so a whole
+ *    decode step can be captured in a CUDA graph.
+ *  - Every call returns a tpla_status.  Arguments are validated BEFORE any
+ *    launch; on failure nothing is launched and tpla_last_error() (thread-local)
+ *    explains.  Asynchronous CUDA faults are reported by the next call that
+ *    synchronises (tpla_sync) as TPLA_ERR_CUDA.  No C++ exception crosses the ABI.
+ */
+#ifndef TPLA_H_
+#define TPLA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t tpla_status;
+enum {
+  TPLA_OK = 0,
+  TPLA_ERR_INVALID_ARG = 1,   /* NULL pointer, bad enum, misaligned pointer            */
+  TPLA_ERR_SHAPE = 2,         /* dimension outside what the kernels support            */
+  TPLA_ERR_DIVISIBILITY = 3,  /* g ∤ k, g ∤ d_c, (k/g) ∤ h_q, d_c not a power of two    */
+  TPLA_ERR_CAPACITY = 4,      /* workspace too small, position beyond the page table    */
+  TPLA_ERR_CUDA = 5,          /* CUDA runtime error (launch or asynchronous fault)      */
+  TPLA_ERR_NCCL = 6,          /* NCCL unavailable or failed                             */
+  TPLA_ERR_UNSUPPORTED = 7    /* valid request this build does not implement            */
+};
+
+/* Orthogonal transform U applied to the latent before slicing (§4.3). */
+enum {
+  TPLA_XFORM_IDENTITY = 0,  /* U = I ("Original" split, Fig. 3)                        */
+  TPLA_XFORM_HADAMARD = 1,  /* U = D H_{d_c} / sqrt(d_c), D = diag(±1) from splitmix64 */
+  TPLA_XFORM_PCA = 2        /* U = eigenvectors of the calibration second moment     */
+};
+
+/* How a cached row is normalised (§4.1). */
+enum {
+  TPLA_RMS_SLICED = 0,  /* sqrt(alpha_j/d_c ||(cU)_j||^2 + eps): the device's slice only */
+  TPLA_RMS_EXACT = 1,   /* sqrt(||c||^2/d_c + eps): full-row RMS, PD-separated prefill  */
+  TPLA_RMS_NONE = 2     /* no normalisation: layout tests (row = bf16 copy of (cU)_j)           */
+};
+
+/* tpla_decode flags */
+enum {
+  TPLA_DECODE_ACCUMULATE = 1  /* y += Õ_j instead of y = Õ_j (single-GPU k-shard emulation) */
+};
+
+/* Model + deployment.  Semantics: PAPER.md §3.1/§3.3 symbols; k devices, g latent groups (§4.4). */
+typedef struct tpla_config {
+  int32_t h_q;      /* query heads                                         */
+  int32_t d_c;      /* latent width (4 d_h in the paper), power of 2 */
+  int32_t d_r;      /* decoupled RoPE width, even                          */
+  int32_t d_h;      /* head dim                                            */
+  int32_t D;        /* hidden size                                         */
+  int32_t k;        /* devices in the tensor-parallel group                */
+  int32_t g;        /* latent groups; g | k, g | d_c, (k/g) | h_q          */
+  int32_t rank;     /* this device, 0 <= rank < k                          */
+  float eps;        /* RMSNorm epsilon                             */
+  float sm_scale;   /* logit scale, one scalar for NoPE and RoPE   */
+} tpla_config;
+
+/* This device's share (group-major: shard j = rank / (k/g), head block i = rank % (k/g)). */
+typedef struct tpla_device_plan {
+  int32_t rank, shard, head_block;
+  int32_t head_begin, head_end;   /* [i·H_loc, (i+1)·H_loc)                        */
+  int32_t lat_begin, lat_end;     /* [j·W_lat, (j+1)·W_lat) of the TRANSFORMED basis */
+  int32_t row_width;              /* W = W_lat + d_r (latent slice ‖ k^PE)  */
+  int32_t h_loc, w_lat;
+} tpla_device_plan;
+
+/* Converted, device-resident weights of one device (caller-allocated device buffers). */
+typedef struct tpla_weights {
+  void* W_UK;         /* bf16 [H_loc, W_lat, d_h]: mu_j · (U^T W_γ W^UK)[lat rows, head h cols]   */
+  void* W_UV;         /* bf16 [H_loc, d_h, W_lat]: (U^T W_γ W^UV)[lat rows, head h cols]^T         */
+  void* W_O;          /* bf16 [D, H_loc·d_h]: (W^O[head rows of block i, :])^T                      */
+  void* xform;        /* fp32: HADAMARD [d_c] signs ±1; PCA [d_c, W_lat] = U[:, lat range]; else NULL */
+  int32_t xform_kind; /* TPLA_XFORM_*                                                              */
+  float alpha_j;      /* Condition 1 constant of this shard                     */
+  float mu_j;         /* Condition 2 constant; already folded into W_UK             */
+} tpla_weights;
+
+/* Paged latent cache of one device: bf16 [num_pages, page_size, row_stride]; a token's row
+ * holds [ĉ_j (W_lat) ‖ k^PE (d_r)] in columns [0, W) and zero padding up to row_stride.
+ * Token t of sequence b lives in page block_table[b·max_pages_per_seq + t / page_size],
+ * row t % page_size.  page_size is a multiple of 64; row_stride a multiple of 64 ≥ W. */
+typedef struct tpla_cache {
+  void* base;                  /* device bf16                                  */
+  const int32_t* block_table;  /* device int32 [batch, max_pages_per_seq]      */
+  int64_t num_pages;
+  int32_t page_size;
+  int32_t max_pages_per_seq;
+  int32_t row_stride;          /* elements                                     */
+  int32_t batch;               /* rows of block_table                          */
+} tpla_cache;
+
+typedef struct tpla_comm tpla_comm; /* opaque: NCCL communicator over the k devices */
+
+/* ---- host-only helpers (no device work) ---------------------------------------- */
+
+const char* tpla_version(void);
+/* Thread-local message for the last non-OK status of this thread ("" if none). */
+const char* tpla_last_error(void);
+/* Number of kernels this library has launched in this process (monotone counter). */
+int64_t tpla_launch_count(void);
+
+/* Device plan of cfg->rank.  Pure integer arithmetic. */
+tpla_status tpla_make_plan(const tpla_config* cfg, tpla_device_plan* out);
+
+/* Hadamard sign diagonal D: out[i] = -1 if bit 63 of splitmix64 output i is set, else +1.
+ * out: host fp32 [d]. */
+tpla_status tpla_hadamard_signs(uint64_t seed, int32_t d, float* out);
+
+/* PCA constants: alpha_j = Σ_all λ / Σ_{slice j} λ, λ in descending order.
+ * lambda: host fp64 [d_c]; alpha_out: host fp32 [g]. */
+tpla_status tpla_pca_alpha(const double* lambda, int32_t d_c, int32_t g, float* alpha_out);
+
+/* Byte sizes of the four device buffers of tpla_weights for cfg->rank (xform = 0 for IDENTITY). */
+tpla_status tpla_weights_bytes(const tpla_config* cfg, int32_t xform_kind, size_t* W_UK, size_t* W_UV,
+                               size_t* W_O, size_t* xform);
+
+/* ---- offline conversion ------------------------------- */
+
+/* Absorb γ and U into W^UK/W^UV (W^UKV_new = U^T W_γ W^UKV), take this device's latent rows
+ * and head block, fold mu_j into the W^UK slice, lay W^UV and W^O out K-major, round to bf16
+ * (RNE) and copy into the caller's device buffers out->W_UK, W_UV, W_O, xform (already set).
+ * Arithmetic in fp64 on the host.
+ *   sign_seed  HADAMARD: seed of D;  U_pca  PCA: host fp32 [d_c, d_c] row-major, column c = c-th
+ *   eigenvector (descending eigenvalue), else NULL;  alpha, mu: host fp32 [g];
+ *   W_UK, W_UV: host bf16 [d_c, h_q·d_h]; gamma: host bf16 [d_c]; W_O: host bf16 [h_q·d_h, D].
+ * Synchronous (returns after the copies completed on `stream`). */
+tpla_status tpla_convert_weights(const tpla_config* cfg, int32_t xform_kind, uint64_t sign_seed,
+                                 const float* U_pca, const float* alpha, const float* mu,
+                                 const uint16_t* W_UK, const uint16_t* W_UV, const uint16_t* gamma,
+                                 const uint16_t* W_O, tpla_weights* out, void* stream);
+
+/* ---- K1: cache write ------------------------------------------------------------- */
+
+/* Append n latent rows.  Row r: c' = c_kv[r]·U; keep (c')_j; normalise per rms_mode; store
+ * bf16(ĉ_j) ‖ k_pe[r] at (seq_idx[r], pos[r]) through the page table.
+ *   c_kv: device bf16 [n, d_c] raw (pre-RMSNorm) latents; k_pe: device bf16 [n, d_r] post-RoPE;
+ *   seq_idx, pos: device int32 [n].  Out-of-range (seq, pos) rows are skipped by the kernel and
+ *   counted in *n_dropped if n_dropped (device int32) is non-NULL. */
+tpla_status tpla_append_kv(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                           const void* c_kv, const void* k_pe, const int32_t* seq_idx, const int32_t* pos,
+                           int32_t n, int32_t rms_mode, int32_t* n_dropped, void* stream);
+
+/* PD-separated prefill: the prompt rows are written to this device's
+ * cache with the EXACT (unsliced) RMS, so decode reuses the MLA prefill cache.  The causal MLA
+ * prefill attention itself is not part of this build (returns TPLA_ERR_UNSUPPORTED if q != NULL). */
+tpla_status tpla_prefill_mla(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                             const void* c_kv, const void* k_pe, const int32_t* seq_idx, const int32_t* pos,
+                             int32_t n, const void* q, void* stream);
+
+/* ---- K2..K5 + C1: decode ---------------------------------------------------------- */
+
+/* Workspace bytes for tpla_decode / tpla_decode_attention with batch B and at most
+ * max_seq_len cached tokens per sequence. */
+tpla_status tpla_decode_workspace_bytes(const tpla_config* cfg, int32_t B, int32_t max_seq_len, size_t* bytes);
+
+/* One decode step of this device (K2, K3, K4, K5) + the all-reduce (C1).
+ *   q_nope: device bf16 [B, h_q, d_h] and q_pe: device bf16 [B, h_q, d_r] hold ALL heads (the
+ *   device reads its head block); seq_lens: device int32 [B], 1 <= seq_lens[b] <= max_seq_len,
+ *   the number of cached tokens (the current token already appended);
+ *   y: device fp32 [B, D]: receives Õ_j (or += with TPLA_DECODE_ACCUMULATE), then, if comm != NULL,
+ *   is all-reduced in place (sum over the k devices);  out: device bf16 [B, D] or NULL:
+ *   bf16(y) after the all-reduce.  A process may hold m of the k ranks: it calls tpla_decode once
+ *   per held rank with TPLA_DECODE_ACCUMULATE after the first and passes comm (world = k/m
+ *   processes) only on the last call, so the all-reduce sums every rank exactly once. */
+tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                        const void* q_nope, const void* q_pe, const int32_t* seq_lens, int32_t B,
+                        int32_t max_seq_len, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,
+                        tpla_comm* comm, void* stream);
+
+/* K3 + K4 only (attention of one shard, Eq. tpla_softmax_one_device without W^VO):
+ *   q_lat: device bf16 [B, H_loc, W_lat] (= Q'_j, mu_j included); q_pe: device bf16 [B, h_q, d_r]
+ *   (all heads); O: device fp32 [B, H_loc, W_lat] = Σ_t p_t ĉ_{j,t};  lse: device fp32 [B, H_loc]
+ *   or NULL: log Σ_t exp(s_t) (natural log, s_t including sm_scale). */
+tpla_status tpla_decode_attention(const tpla_config* cfg, const tpla_cache* cache, const void* q_lat,
+                                  const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t max_seq_len,
+                                  void* ws, size_t ws_bytes, float* O, float* lse, void* stream);
+
+/* ---- C1: communicator -------------------------------------------------------------- */
+
+/* 128-byte NCCL unique id for rank 0 to broadcast (e.g. over a torch.distributed group). */
+tpla_status tpla_comm_unique_id(void* out128);
+/* Join the k-device communicator (blocking until all ranks join).  The current CUDA device
+ * must already be this rank's GPU. */
+tpla_status tpla_comm_init(tpla_comm** out, const void* unique_id128, int32_t world, int32_t rank);
+tpla_status tpla_comm_destroy(tpla_comm* comm);
+
+/* Synchronise `stream` and report any asynchronous CUDA fault. */
+tpla_status tpla_sync(void* stream);
+
+/* ---- measurement: per-kernel device time --------------------------------------------- */
+
+/* When on != 0, every kernel launch of this library is bracketed by two CUDA events recorded
+ * on its launching stream (no device work is added).  Host-side bookkeeping only. */
+tpla_status tpla_profile_enable(int32_t on);
+/* Wait for the recorded events and accumulate their elapsed times per kernel name. */
+tpla_status tpla_profile_collect(void);
+/* Number of distinct kernel names accumulated so far. */
+int32_t tpla_profile_count(void);
+/* Entry i: name (host buffer of 64 bytes), total milliseconds, number of launches. */
+tpla_status tpla_profile_get(int32_t i, char* name64, double* total_ms, int64_t* launches);
+/* Drop all accumulated and pending records. */
+tpla_status tpla_profile_reset(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPLA_H_ */

@@ -84,6 +84,22 @@ def absorb_query(q_nope_b, dw: DeviceWeights):
     return np.einsum("hld,hd->hl", dw.W_UK, q_nope_b)
 
 
+def shard_attention(Qp, qpe, rows, w_lat: int, sm_scale: float):
+    """Attention of one shard for one sequence (Eq. tpla_softmax_one_device P:137-138 with the
+    replicated RoPE logits of P:238-242): Qp [H, W_lat] (mu_j included), qpe [H, d_r],
+    rows [S, W_lat + d_r].  Returns O [H, W_lat] = softmax(s) ĉ_j, lse [H] = log Σ_t exp(s_t),
+    p [H, S] and the RoPE logits [H, S]."""
+    c_hat = rows[:, :w_lat]                     # ĉ_j  [S, W_lat]
+    kpe = rows[:, w_lat:]                       # k^PE [S, d_r] (replicated, P:238)
+    nope = Qp @ c_hat.T                         # Q'_j ĉ_jᵀ (mu_j already in Q'_j)
+    rope = qpe @ kpe.T                          # q^PE k^PEᵀ, unscaled by mu (R6)
+    s = sm_scale * (nope + rope)
+    p = softmax(s)                              # per-shard softmax (P:137-138, P:242)
+    smax = np.max(s, axis=1)
+    lse = smax + np.log(np.sum(np.exp(s - smax[:, None]), axis=1))
+    return p @ c_hat, lse, p, rope
+
+
 def decode_device(q_nope, q_pe, rows, dw: DeviceWeights, plan: DevicePlan, *, sm_scale, return_parts=False):
     """One device's decode step over a batch (Eq. tpla_softmax_one_device).
 
@@ -102,13 +118,8 @@ def decode_device(q_nope, q_pe, rows, dw: DeviceWeights, plan: DevicePlan, *, sm
     P_all, R_all = [], []
     heads = slice(plan.head_begin, plan.head_end)
     for b in range(B):
-        c_hat = rows[b][:, :W_lat]                  # ĉ_j  [S, W_lat]
-        kpe = rows[b][:, W_lat:]                    # k^PE [S, d_r] (replicated)
         Qp = absorb_query(q_nope[b, heads], dw)     # Q'_j [H, W_lat]
-        nope = Qp @ c_hat.T                         # Q'_j ĉ_jᵀ (mu_j already in W^UK'_j)
-        rope = q_pe[b, heads] @ kpe.T               # q^PE k^PEᵀ, unscaled by mu (R6)
-        p = softmax(sm_scale * (nope + rope))       # per-shard softmax
-        O = p @ c_hat                               # O_j = softmax(·) ĉ_j   [H, W_lat]
+        O, _, p, rope = shard_attention(Qp, q_pe[b, heads], rows[b], W_lat, sm_scale)   # O_j [H, W_lat]
         v = np.einsum("hl,hld->hd", O, dw.W_UV)     # O_j W^UV'_j per head   [H, d_h]
         y[b] = v.reshape(H * d_h) @ dw.W_O          # Õ_j = O_j W^VO_j
         O_all[b] = O

@@ -1,0 +1,84 @@
+// Internal interface between the C-ABI layer (tpla_abi.cpp) and the CUDA kernels.
+// Not installed; the public surface is include/tpla.h.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/tpla.h"
+
+namespace tpla {
+
+extern std::atomic<int64_t> g_launches;
+extern std::atomic<int> g_profile_on;
+
+// Wraps one kernel launch: counts it (tpla_launch_count) and, when profiling is enabled
+// (tpla_profile_enable), brackets it with CUDA events on the launching stream.
+struct KernelScope {
+  KernelScope(const char* name, cudaStream_t s);
+  ~KernelScope();
+  int slot = -1;
+  cudaStream_t stream;
+};
+
+// Resolved per-device problem geometry (validated).
+struct Geom {
+  int h_q, d_c, d_r, d_h, D;
+  int k, g, rank;
+  int h_loc, w_lat, W;          // W = w_lat + d_r
+  int head_begin, lat_begin;
+  float eps, sm_scale;
+};
+
+// Split-K work decomposition of K3.
+struct SplitPlan {
+  int n_split;      // splits per sequence
+  int chunk;        // tokens per split (multiple of 64)
+};
+
+// Workspace layout of tpla_decode (byte offsets, all 256-aligned).
+struct WsLayout {
+  size_t q_lat;     // bf16 [B, H_loc, W_lat]   (Q'_j)
+  size_t o_part;    // fp32 [B*n_split, H_loc, W_lat]
+  size_t ml_part;   // fp32 [B*n_split, H_loc, 2] (m, l)
+  size_t o_lat;     // bf16 [B, H_loc, W_lat]   (combined O_j)
+  size_t v;         // bf16 [B, H_loc*d_h]
+  size_t y_part;    // fp32 [kslices, B, D]
+  size_t total;
+  int kslices;
+};
+
+SplitPlan choose_split(int B, int max_seq_len);
+WsLayout ws_layout(const Geom& g, int B, int max_seq_len);
+
+// ---- kernels (each returns cudaGetLastError() after launch) ----
+cudaError_t launch_append_kv(const Geom& g, int xform_kind, const float* xform, float alpha_j,
+                             const tpla_cache& cache, const uint16_t* c_kv, const uint16_t* k_pe,
+                             const int32_t* seq_idx, const int32_t* pos, int n, int rms_mode,
+                             int32_t* n_dropped, cudaStream_t s);
+
+// out[b, h, r] = sum_c W[h, r, c] * x[b, h, c]     (K2 with R=W_lat,C=d_h; K5a with R=d_h,C=W_lat)
+// x has row stride x_head_stride elements between heads and x_batch_stride between batches.
+cudaError_t launch_head_gemv(const char* name, const uint16_t* W, const uint16_t* x, long x_batch_stride, int H,
+                             int R, int C, int B, uint16_t* out_bf16, cudaStream_t s);
+
+cudaError_t launch_decode_attn(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat,
+                               const uint16_t* q_pe, const int32_t* seq_lens, int B, const SplitPlan& sp,
+                               float* o_part, float* ml_part, cudaStream_t s);
+
+cudaError_t launch_combine(const Geom& g, int B, const SplitPlan& sp, const float* o_part, const float* ml_part,
+                           uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s);
+
+// y_part[ks, b, n] = sum_{k in slice ks} Wt[n, k] * v[b, k]; Wt [N, K] bf16, v [B, K] bf16.
+cudaError_t launch_skinny_gemm(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, int kslices,
+                               float* y_part, cudaStream_t s);
+
+// y[b, n] (=|+=) sum_ks y_part[ks, b, n]
+cudaError_t launch_reduce_slices(const float* y_part, int kslices, int B, int N, float* y, bool accumulate,
+                                 cudaStream_t s);
+
+cudaError_t launch_cast_bf16(const float* y, long n, uint16_t* out, cudaStream_t s);
+
+}  // namespace tpla

@@ -1,0 +1,564 @@
+// C-ABI entry points of libtpla.so (include/tpla.h): validation, host-side conversion,
+// workspace carving, kernel sequencing and the NCCL communicator.
+//
+// Citations "P:n" refer to lines of the paper text.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+#include "nccl.h"
+
+namespace tpla {
+std::atomic<int64_t> g_launches{0};
+}
+
+using namespace tpla;
+
+namespace {
+
+thread_local std::string t_err;
+
+tpla_status fail(tpla_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return st;
+}
+
+tpla_status ok() {
+  t_err.clear();
+  return TPLA_OK;
+}
+
+tpla_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(TPLA_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define TPLA_CUDA(call, where)                    \
+  do {                                            \
+    cudaError_t e_ = (call);                      \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Validate cfg and resolve this device's geometry.
+tpla_status make_geom(const tpla_config* c, Geom* g) {
+  if (!c || !g) return fail(TPLA_ERR_INVALID_ARG, "NULL config");
+  if (c->h_q < 1 || c->d_c < 1 || c->d_r < 0 || c->d_h < 1 || c->D < 1 || c->k < 1 || c->g < 1)
+    return fail(TPLA_ERR_SHAPE, "non-positive dimension");
+  if (c->k % c->g) return fail(TPLA_ERR_DIVISIBILITY, "g=%d must divide k=%d", c->g, c->k);
+  if (c->d_c % c->g) return fail(TPLA_ERR_DIVISIBILITY, "g=%d must divide d_c=%d", c->g, c->d_c);
+  int per_group = c->k / c->g;
+  if (c->h_q % per_group) return fail(TPLA_ERR_DIVISIBILITY, "k/g=%d must divide h_q=%d", per_group, c->h_q);
+  if (c->rank < 0 || c->rank >= c->k) return fail(TPLA_ERR_INVALID_ARG, "rank %d outside [0,%d)", c->rank, c->k);
+  if (c->d_r % 2) return fail(TPLA_ERR_SHAPE, "d_r must be even");
+  if (!(c->eps >= 0.f) || !(c->sm_scale > 0.f)) return fail(TPLA_ERR_INVALID_ARG, "eps/sm_scale out of range");
+  g->h_q = c->h_q; g->d_c = c->d_c; g->d_r = c->d_r; g->d_h = c->d_h; g->D = c->D;
+  g->k = c->k; g->g = c->g; g->rank = c->rank;
+  int j = c->rank / per_group, i = c->rank % per_group;
+  g->h_loc = c->h_q / per_group;
+  g->w_lat = c->d_c / c->g;
+  g->W = g->w_lat + c->d_r;
+  g->head_begin = i * g->h_loc;
+  g->lat_begin = j * g->w_lat;
+  g->eps = c->eps;
+  g->sm_scale = c->sm_scale;
+  return TPLA_OK;
+}
+
+// Kernel-side limits of this build (checked before any launch).
+tpla_status check_kernel_shapes(const Geom& g) {
+  if (!is_pow2(g.d_c) || g.d_c < 32 || g.d_c > 1024)
+    return fail(TPLA_ERR_SHAPE, "d_c=%d: kernels need a power of two in [32, 1024]", g.d_c);
+  if (g.w_lat % 32 || g.w_lat > 256)
+    return fail(TPLA_ERR_UNSUPPORTED, "W_lat=%d: decode kernels support multiples of 32 up to 256", g.w_lat);
+  if (!(g.d_r == 16 || g.d_r == 64)) return fail(TPLA_ERR_UNSUPPORTED, "d_r=%d: decode kernels support 16 or 64", g.d_r);
+  if (g.h_loc > 128) return fail(TPLA_ERR_UNSUPPORTED, "H_loc=%d > 128", g.h_loc);
+  if (g.d_h % 16 || g.d_h > 256) return fail(TPLA_ERR_UNSUPPORTED, "d_h=%d: multiple of 16 up to 256", g.d_h);
+  if ((g.h_loc * g.d_h) % 8) return fail(TPLA_ERR_UNSUPPORTED, "H_loc*d_h must be a multiple of 8");
+  if (g.D % 8) return fail(TPLA_ERR_UNSUPPORTED, "D must be a multiple of 8");
+  return TPLA_OK;
+}
+
+tpla_status check_cache(const Geom& g, const tpla_cache* c) {
+  if (!c || !c->base || !c->block_table) return fail(TPLA_ERR_INVALID_ARG, "NULL cache");
+  if (!aligned16(c->base)) return fail(TPLA_ERR_INVALID_ARG, "cache base not 16-byte aligned");
+  if (c->page_size < 64 || c->page_size % 64) return fail(TPLA_ERR_SHAPE, "page_size must be a positive multiple of 64");
+  if (c->row_stride < g.W || c->row_stride % 64) return fail(TPLA_ERR_SHAPE, "row_stride=%d must be a multiple of 64 >= W=%d", c->row_stride, g.W);
+  if (c->num_pages < 1 || c->max_pages_per_seq < 1 || c->batch < 1) return fail(TPLA_ERR_SHAPE, "empty cache");
+  return TPLA_OK;
+}
+
+uint64_t splitmix64_next(uint64_t& state) {
+  state += 0x9E3779B97F4A7C15ull;
+  uint64_t z = state;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+double bf16_to_double(uint16_t b) {
+  uint32_t u = static_cast<uint32_t>(b) << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+uint16_t double_to_bf16(double x) {
+  // nearest bf16 (8 significant bits), ties to even, taken directly on the fp64 value
+  if (x == 0.0) return signbit(x) ? 0x8000u : 0u;
+  int e;
+  double m = frexp(x, &e);                 // x = m 2^e, 0.5 <= |m| < 1
+  double r = nearbyint(m * 256.0);         // FE_TONEAREST: ties to even
+  float f = static_cast<float>(ldexp(r / 256.0, e));
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+template <class F>
+void parallel_for(int n, F f) {
+  int nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  nt = std::min(nt, n);
+  if (nt <= 1) { for (int i = 0; i < n; ++i) f(i); return; }
+  std::vector<std::thread> th;
+  std::atomic<int> next{0};
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&] { for (int i; (i = next.fetch_add(1)) < n;) f(i); });
+  for (auto& x : th) x.join();
+}
+
+// ---- NCCL, loaded at run time (the library must load without it) ----
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  const char* env = getenv("TPLA_NCCL_LIB");
+  const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+  void* h = nullptr;
+  for (const char* n : names) {
+    if (!n) continue;
+    h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (h) break;
+  }
+  if (!h) return false;
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy && g_nccl.GetErrorString;
+  return g_nccl.ok;
+}
+
+}  // namespace
+
+struct tpla_comm {
+  ncclComm_t comm;
+  int world, rank;
+};
+
+namespace tpla {
+
+SplitPlan choose_split(int B, int max_seq_len) {
+  // Fixed split of every sequence into n_split chunks of 64-token multiples, sized from the
+  // capacity bound (not the live lengths) so the launch shape is graph-capturable:
+  // B * n_split ≈ 2 waves of 148 SMs.
+  const int kSMs = 148;
+  int tiles = (max_seq_len + 63) / 64;
+  int want = std::max(1, (2 * kSMs + B - 1) / B);
+  int n_split = std::max(1, std::min(tiles, want));
+  int chunk = ((tiles + n_split - 1) / n_split) * 64;
+  n_split = (max_seq_len + chunk - 1) / chunk;
+  return SplitPlan{n_split, chunk};
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+WsLayout ws_layout(const Geom& g, int B, int max_seq_len) {
+  WsLayout L{};
+  SplitPlan sp = choose_split(B, max_seq_len);
+  int K = g.h_loc * g.d_h;
+  // split K = H_loc*d_h of the W^O GEMM into equal 64-multiples (at most 16) to fill the SMs
+  L.kslices = std::max(1, std::min(K / 64, 16));
+  while (L.kslices > 1 && (K / 64) % L.kslices) --L.kslices;
+  if (K % (64 * L.kslices)) L.kslices = 1;
+  size_t off = 0;
+  L.q_lat = off;   off += align256(size_t(B) * g.h_loc * g.w_lat * 2);
+  L.o_part = off;  off += align256(size_t(B) * sp.n_split * g.h_loc * g.w_lat * 4);
+  L.ml_part = off; off += align256(size_t(B) * sp.n_split * g.h_loc * 2 * 4);
+  L.o_lat = off;   off += align256(size_t(B) * g.h_loc * g.w_lat * 2);
+  L.v = off;       off += align256(size_t(B) * K * 2);
+  L.y_part = off;  off += align256(size_t(L.kslices) * B * g.D * 4);
+  L.total = off;
+  return L;
+}
+
+}  // namespace tpla
+
+// =====================================================================================
+extern "C" {
+
+const char* tpla_version(void) { return "tpla-b200 0.1 (sm_100a)"; }
+const char* tpla_last_error(void) { return t_err.c_str(); }
+int64_t tpla_launch_count(void) { return g_launches.load(); }
+
+tpla_status tpla_make_plan(const tpla_config* cfg, tpla_device_plan* out) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return st;
+  if (!out) return fail(TPLA_ERR_INVALID_ARG, "NULL plan");
+  out->rank = g.rank;
+  out->shard = g.lat_begin / g.w_lat;
+  out->head_block = g.head_begin / g.h_loc;
+  out->head_begin = g.head_begin;
+  out->head_end = g.head_begin + g.h_loc;
+  out->lat_begin = g.lat_begin;
+  out->lat_end = g.lat_begin + g.w_lat;
+  out->row_width = g.W;
+  out->h_loc = g.h_loc;
+  out->w_lat = g.w_lat;
+  return ok();
+}
+
+tpla_status tpla_hadamard_signs(uint64_t seed, int32_t d, float* out) {
+  if (!out || d < 1) return fail(TPLA_ERR_INVALID_ARG, "bad arguments");
+  uint64_t state = seed;
+  for (int i = 0; i < d; ++i) out[i] = (splitmix64_next(state) >> 63) ? -1.f : 1.f;
+  return ok();
+}
+
+tpla_status tpla_pca_alpha(const double* lambda, int32_t d_c, int32_t g, float* alpha_out) {
+  if (!lambda || !alpha_out || d_c < 1 || g < 1) return fail(TPLA_ERR_INVALID_ARG, "bad arguments");
+  if (d_c % g) return fail(TPLA_ERR_DIVISIBILITY, "g must divide d_c");
+  double total = 0;
+  for (int i = 0; i < d_c; ++i) total += lambda[i];
+  int w = d_c / g;
+  for (int j = 0; j < g; ++j) {
+    double s = 0;
+    for (int i = j * w; i < (j + 1) * w; ++i) s += lambda[i];
+    if (!(s > 0)) return fail(TPLA_ERR_INVALID_ARG, "slice %d has no energy", j);
+    alpha_out[j] = static_cast<float>(total / s);
+  }
+  return ok();
+}
+
+tpla_status tpla_weights_bytes(const tpla_config* cfg, int32_t xform_kind, size_t* W_UK, size_t* W_UV,
+                               size_t* W_O, size_t* xform) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return st;
+  if (W_UK) *W_UK = size_t(g.h_loc) * g.w_lat * g.d_h * 2;
+  if (W_UV) *W_UV = size_t(g.h_loc) * g.d_h * g.w_lat * 2;
+  if (W_O) *W_O = size_t(g.D) * g.h_loc * g.d_h * 2;
+  if (xform) {
+    if (xform_kind == TPLA_XFORM_HADAMARD) *xform = size_t(g.d_c) * 4;
+    else if (xform_kind == TPLA_XFORM_PCA) *xform = size_t(g.d_c) * g.w_lat * 4;
+    else if (xform_kind == TPLA_XFORM_IDENTITY) *xform = 0;
+    else return fail(TPLA_ERR_INVALID_ARG, "bad xform_kind");
+  }
+  return ok();
+}
+
+tpla_status tpla_convert_weights(const tpla_config* cfg, int32_t xform_kind, uint64_t sign_seed,
+                                 const float* U_pca, const float* alpha, const float* mu,
+                                 const uint16_t* W_UK, const uint16_t* W_UV, const uint16_t* gamma,
+                                 const uint16_t* W_O, tpla_weights* out, void* stream) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return st;
+  if (!alpha || !mu || !W_UK || !W_UV || !gamma || !W_O || !out || !out->W_UK || !out->W_UV || !out->W_O)
+    return fail(TPLA_ERR_INVALID_ARG, "NULL argument");
+  if (xform_kind == TPLA_XFORM_HADAMARD && !is_pow2(g.d_c))
+    return fail(TPLA_ERR_DIVISIBILITY, "Hadamard needs d_c a power of two (P:274)");
+  if (xform_kind == TPLA_XFORM_PCA && !U_pca) return fail(TPLA_ERR_INVALID_ARG, "PCA needs U_pca");
+  if (xform_kind < 0 || xform_kind > 2) return fail(TPLA_ERR_INVALID_ARG, "bad xform_kind");
+  if (xform_kind != TPLA_XFORM_IDENTITY && !out->xform) return fail(TPLA_ERR_INVALID_ARG, "NULL xform buffer");
+  const int d_c = g.d_c, d_h = g.d_h, hq = g.h_q, H = g.h_loc, WL = g.w_lat, D = g.D;
+  const int shard = g.lat_begin / WL;
+  const double mu_j = mu[shard];
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+  std::vector<double> signs(d_c, 1.0);
+  if (xform_kind == TPLA_XFORM_HADAMARD) {
+    uint64_t state = sign_seed;
+    for (int i = 0; i < d_c; ++i) signs[i] = (splitmix64_next(state) >> 63) ? -1.0 : 1.0;
+  }
+  // W^UKV_new = U^T W_γ W^UKV, only for the device's latent rows and head columns.
+  // U^T (x) for Hadamard: U = D H / sqrt(d) so U^T x = H (D x) / sqrt(d) (H symmetric).
+  std::vector<uint16_t> uk(size_t(H) * WL * d_h), uv(size_t(H) * d_h * WL);
+  const double inv_sqrt_d = 1.0 / sqrt(double(d_c));
+  parallel_for(H * d_h, [&](int col_local) {
+    const int h = col_local / d_h, e = col_local % d_h;
+    const size_t col = size_t(g.head_begin + h) * d_h + e;
+    std::vector<double> a(d_c), b(d_c), ta(WL), tb(WL);
+    for (int r = 0; r < d_c; ++r) {
+      double gm = bf16_to_double(gamma[r]);
+      a[r] = gm * bf16_to_double(W_UK[size_t(r) * hq * d_h + col]);
+      b[r] = gm * bf16_to_double(W_UV[size_t(r) * hq * d_h + col]);
+    }
+    if (xform_kind == TPLA_XFORM_HADAMARD) {
+      for (int r = 0; r < d_c; ++r) { a[r] *= signs[r]; b[r] *= signs[r]; }
+      for (int len = 1; len < d_c; len <<= 1)
+        for (int i = 0; i < d_c; i += 2 * len)
+          for (int q = i; q < i + len; ++q) {
+            double x = a[q], y = a[q + len];
+            a[q] = x + y; a[q + len] = x - y;
+            x = b[q]; y = b[q + len];
+            b[q] = x + y; b[q + len] = x - y;
+          }
+      for (int l = 0; l < WL; ++l) { ta[l] = a[g.lat_begin + l] * inv_sqrt_d; tb[l] = b[g.lat_begin + l] * inv_sqrt_d; }
+    } else if (xform_kind == TPLA_XFORM_PCA) {
+      for (int l = 0; l < WL; ++l) {
+        double sa = 0, sb = 0;
+        for (int r = 0; r < d_c; ++r) {
+          double u = U_pca[size_t(r) * d_c + g.lat_begin + l];   // (U^T)[l][r] = U[r][l]
+          sa += u * a[r];
+          sb += u * b[r];
+        }
+        ta[l] = sa; tb[l] = sb;
+      }
+    } else {
+      for (int l = 0; l < WL; ++l) { ta[l] = a[g.lat_begin + l]; tb[l] = b[g.lat_begin + l]; }
+    }
+    for (int l = 0; l < WL; ++l) {
+      uk[(size_t(h) * WL + l) * d_h + e] = double_to_bf16(mu_j * ta[l]);   // mu_j folded
+      uv[(size_t(h) * d_h + e) * WL + l] = double_to_bf16(tb[l]);
+    }
+  });
+  // W^O rows of head block i, transposed to [D, H*d_h] (K-major for the up-projection GEMM)
+  const int K = H * d_h;
+  std::vector<uint16_t> wo(size_t(D) * K);
+  parallel_for(K, [&](int kk) {
+    const uint16_t* src = W_O + (size_t(g.head_begin) * d_h + kk) * D;
+    for (int n = 0; n < D; ++n) wo[size_t(n) * K + kk] = src[n];
+  });
+  std::vector<float> xf;
+  if (xform_kind == TPLA_XFORM_HADAMARD) {
+    xf.resize(d_c);
+    for (int i = 0; i < d_c; ++i) xf[i] = static_cast<float>(signs[i]);
+  } else if (xform_kind == TPLA_XFORM_PCA) {
+    xf.resize(size_t(d_c) * WL);
+    for (int r = 0; r < d_c; ++r)
+      for (int l = 0; l < WL; ++l) xf[size_t(r) * WL + l] = U_pca[size_t(r) * d_c + g.lat_begin + l];
+  }
+  TPLA_CUDA(cudaMemcpyAsync(out->W_UK, uk.data(), uk.size() * 2, cudaMemcpyHostToDevice, s), "copy W_UK");
+  TPLA_CUDA(cudaMemcpyAsync(out->W_UV, uv.data(), uv.size() * 2, cudaMemcpyHostToDevice, s), "copy W_UV");
+  TPLA_CUDA(cudaMemcpyAsync(out->W_O, wo.data(), wo.size() * 2, cudaMemcpyHostToDevice, s), "copy W_O");
+  if (!xf.empty())
+    TPLA_CUDA(cudaMemcpyAsync(out->xform, xf.data(), xf.size() * 4, cudaMemcpyHostToDevice, s), "copy xform");
+  TPLA_CUDA(cudaStreamSynchronize(s), "convert sync");
+  out->xform_kind = xform_kind;
+  out->alpha_j = alpha[shard];
+  out->mu_j = mu[shard];
+  return ok();
+}
+
+static tpla_status append_common(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                                 const void* c_kv, const void* k_pe, const int32_t* seq_idx, const int32_t* pos,
+                                 int32_t n, int32_t rms_mode, int32_t* n_dropped, void* stream) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return st;
+  if ((st = check_cache(g, cache))) return st;
+  if (!is_pow2(g.d_c) || g.d_c < 32 || g.d_c > 1024)
+    return fail(TPLA_ERR_SHAPE, "d_c=%d: cache-write kernel needs a power of two in [32, 1024]", g.d_c);
+  if (g.d_r % 2) return fail(TPLA_ERR_SHAPE, "d_r must be even");
+  if (!w) return fail(TPLA_ERR_INVALID_ARG, "NULL weights");
+  if (w->xform_kind < 0 || w->xform_kind > 2) return fail(TPLA_ERR_INVALID_ARG, "bad xform_kind");
+  if (w->xform_kind != TPLA_XFORM_IDENTITY && !w->xform) return fail(TPLA_ERR_INVALID_ARG, "NULL xform");
+  if (rms_mode < 0 || rms_mode > 2) return fail(TPLA_ERR_INVALID_ARG, "bad rms_mode");
+  if (rms_mode == TPLA_RMS_SLICED && !(w->alpha_j > 0.f)) return fail(TPLA_ERR_INVALID_ARG, "alpha_j must be > 0");
+  if (n < 0) return fail(TPLA_ERR_INVALID_ARG, "n < 0");
+  if (n == 0) return ok();
+  if (!c_kv || !k_pe || !seq_idx || !pos) return fail(TPLA_ERR_INVALID_ARG, "NULL input");
+  if (!aligned16(c_kv)) return fail(TPLA_ERR_INVALID_ARG, "c_kv not 16-byte aligned");
+  cudaError_t e = launch_append_kv(g, w->xform_kind, static_cast<const float*>(w->xform), w->alpha_j, *cache,
+                                   static_cast<const uint16_t*>(c_kv), static_cast<const uint16_t*>(k_pe), seq_idx,
+                                   pos, n, rms_mode, n_dropped, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "append_kv launch");
+  return ok();
+}
+
+tpla_status tpla_append_kv(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                           const void* c_kv, const void* k_pe, const int32_t* seq_idx, const int32_t* pos,
+                           int32_t n, int32_t rms_mode, int32_t* n_dropped, void* stream) {
+  return append_common(cfg, w, cache, c_kv, k_pe, seq_idx, pos, n, rms_mode, n_dropped, stream);
+}
+
+tpla_status tpla_prefill_mla(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                             const void* c_kv, const void* k_pe, const int32_t* seq_idx, const int32_t* pos,
+                             int32_t n, const void* q, void* stream) {
+  if (q) return fail(TPLA_ERR_UNSUPPORTED, "MLA prefill attention is not part of this build (SURVEY f1)");
+  return append_common(cfg, w, cache, c_kv, k_pe, seq_idx, pos, n, TPLA_RMS_EXACT, nullptr, stream);
+}
+
+tpla_status tpla_decode_workspace_bytes(const tpla_config* cfg, int32_t B, int32_t max_seq_len, size_t* bytes) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return st;
+  if (B < 1 || max_seq_len < 1 || !bytes) return fail(TPLA_ERR_INVALID_ARG, "bad B/max_seq_len");
+  *bytes = ws_layout(g, B, max_seq_len).total;
+  return ok();
+}
+
+static tpla_status check_decode_common(const Geom& g, const tpla_cache* cache, const void* q_pe,
+                                       const int32_t* seq_lens, int B, int max_seq_len) {
+  tpla_status st;
+  if ((st = check_kernel_shapes(g))) return st;
+  if ((st = check_cache(g, cache))) return st;
+  if (B < 1 || B > cache->batch) return fail(TPLA_ERR_SHAPE, "B=%d outside [1, cache batch %d]", B, cache->batch);
+  if (max_seq_len < 1 || int64_t(max_seq_len) > int64_t(cache->max_pages_per_seq) * cache->page_size)
+    return fail(TPLA_ERR_CAPACITY, "max_seq_len=%d exceeds page-table capacity", max_seq_len);
+  if (!q_pe || !seq_lens) return fail(TPLA_ERR_INVALID_ARG, "NULL input");
+  if (!aligned16(q_pe)) return fail(TPLA_ERR_INVALID_ARG, "q_pe not 16-byte aligned");
+  return TPLA_OK;
+}
+
+tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                        const void* q_nope, const void* q_pe, const int32_t* seq_lens, int32_t B,
+                        int32_t max_seq_len, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,
+                        tpla_comm* comm, void* stream) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return st;
+  if ((st = check_decode_common(g, cache, q_pe, seq_lens, B, max_seq_len))) return st;
+  if (!w || !w->W_UK || !w->W_UV || !w->W_O) return fail(TPLA_ERR_INVALID_ARG, "NULL weights");
+  if (!q_nope || !y || !ws) return fail(TPLA_ERR_INVALID_ARG, "NULL q_nope/y/ws");
+  if (!aligned16(q_nope) || !aligned16(ws) || !aligned16(y)) return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
+  // A process may hold several of the k ranks (they accumulate into y before the all-reduce),
+  // so the communicator spans k/m processes for some m >= 1.
+  if (comm && (g.k % comm->world))
+    return fail(TPLA_ERR_INVALID_ARG, "communicator world %d does not divide k=%d", comm->world, g.k);
+  WsLayout L = ws_layout(g, B, max_seq_len);
+  if (ws_bytes < L.total) return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, L.total);
+  SplitPlan sp = choose_split(B, max_seq_len);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(ws);
+  auto* q_lat = reinterpret_cast<uint16_t*>(base + L.q_lat);
+  auto* o_part = reinterpret_cast<float*>(base + L.o_part);
+  auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
+  auto* o_lat = reinterpret_cast<uint16_t*>(base + L.o_lat);
+  auto* v = reinterpret_cast<uint16_t*>(base + L.v);
+  auto* y_part = reinterpret_cast<float*>(base + L.y_part);
+  const auto* qn = static_cast<const uint16_t*>(q_nope);
+  cudaError_t e;
+  // K2: Q'_j[b,h,:] = W^UK'_j[h] q[b,h,:]   (mu_j folded)
+  e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK), qn + size_t(g.head_begin) * g.d_h,
+                       long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h, B, q_lat, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K2 absorb_q");
+  // K3: per-shard split-K flash decoding (Eq. tpla_softmax_one_device)
+  e = launch_decode_attn(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, sp, o_part, ml_part, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K3 decode_attn");
+  // K4: combine the splits -> O_j
+  e = launch_combine(g, B, sp, o_part, ml_part, o_lat, nullptr, nullptr, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K4 combine");
+  // K5a: v[b,h,:] = W^UV'_j[h]^T-applied O_j  (W^VO factored)
+  e = launch_head_gemv("K5_W_UV", static_cast<const uint16_t*>(w->W_UV), o_lat, long(g.h_loc) * g.w_lat, g.h_loc, g.d_h,
+                       g.w_lat, B, v, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K5a W_UV");
+  // K5b: Õ_j = v W^O_rows
+  e = launch_skinny_gemm(static_cast<const uint16_t*>(w->W_O), v, g.D, g.h_loc * g.d_h, B, L.kslices, y_part, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K5b W_O");
+  e = launch_reduce_slices(y_part, L.kslices, B, g.D, y, (flags & TPLA_DECODE_ACCUMULATE) != 0, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K5b reduce");
+  // C1: O = AllReduce(Σ_r Õ_r)
+  if (comm) {
+    ncclResult_t r = g_nccl.AllReduce(y, y, size_t(B) * g.D, ncclFloat32, ncclSum, comm->comm, s);
+    if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
+  }
+  if (out) {
+    if (!aligned16(out)) return fail(TPLA_ERR_INVALID_ARG, "out misaligned");
+    e = launch_cast_bf16(y, long(B) * g.D, static_cast<uint16_t*>(out), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cast");
+  }
+  return ok();
+}
+
+tpla_status tpla_decode_attention(const tpla_config* cfg, const tpla_cache* cache, const void* q_lat,
+                                  const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t max_seq_len,
+                                  void* ws, size_t ws_bytes, float* O, float* lse, void* stream) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return st;
+  if ((st = check_decode_common(g, cache, q_pe, seq_lens, B, max_seq_len))) return st;
+  if (!q_lat || !O || !ws) return fail(TPLA_ERR_INVALID_ARG, "NULL q_lat/O/ws");
+  if (!aligned16(q_lat) || !aligned16(ws)) return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
+  WsLayout L = ws_layout(g, B, max_seq_len);
+  if (ws_bytes < L.total) return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, L.total);
+  SplitPlan sp = choose_split(B, max_seq_len);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(ws);
+  auto* o_part = reinterpret_cast<float*>(base + L.o_part);
+  auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
+  cudaError_t e = launch_decode_attn(g, *cache, static_cast<const uint16_t*>(q_lat),
+                                     static_cast<const uint16_t*>(q_pe), seq_lens, B, sp, o_part, ml_part, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K3 decode_attn");
+  e = launch_combine(g, B, sp, o_part, ml_part, nullptr, O, lse, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K4 combine");
+  return ok();
+}
+
+tpla_status tpla_comm_unique_id(void* out128) {
+  if (!out128) return fail(TPLA_ERR_INVALID_ARG, "NULL id buffer");
+  if (!load_nccl()) return fail(TPLA_ERR_NCCL, "libnccl.so.2 not loadable (set TPLA_NCCL_LIB)");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclGetUniqueId: %s", g_nccl.GetErrorString(r));
+  memcpy(out128, &id, 128);
+  return ok();
+}
+
+tpla_status tpla_comm_init(tpla_comm** out, const void* unique_id128, int32_t world, int32_t rank) {
+  if (!out || !unique_id128 || world < 1 || rank < 0 || rank >= world) return fail(TPLA_ERR_INVALID_ARG, "bad arguments");
+  if (!load_nccl()) return fail(TPLA_ERR_NCCL, "libnccl.so.2 not loadable (set TPLA_NCCL_LIB)");
+  ncclUniqueId id;
+  memcpy(&id, unique_id128, 128);
+  ncclComm_t c;
+  ncclResult_t r = g_nccl.CommInitRank(&c, world, id, rank);
+  if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+  *out = new tpla_comm{c, world, rank};
+  return ok();
+}
+
+tpla_status tpla_comm_destroy(tpla_comm* comm) {
+  if (!comm) return ok();
+  if (g_nccl.ok) g_nccl.CommDestroy(comm->comm);
+  delete comm;
+  return ok();
+}
+
+tpla_status tpla_sync(void* stream) {
+  cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tpla_sync");
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "tpla_sync");
+  return ok();
+}
+
+}  // extern "C"

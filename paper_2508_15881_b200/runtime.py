@@ -1,0 +1,131 @@
+"""Device-side state of one TPLA rank: converted weights, paged latent cache, workspace.
+
+PyTorch is used only to allocate device memory and to name streams; every step of the
+decode path runs inside libtpla.so (see ``_abi``).  This module is marshalling:
+it sizes and allocates buffers, fills the C structs and calls the C entry points.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+import torch
+
+from . import _abi as abi
+
+
+@dataclasses.dataclass(frozen=True)
+class LayerSpec:
+    h_q: int
+    d_c: int
+    d_r: int
+    d_h: int
+    D: int
+    eps: float = 1e-6
+    sm_scale: float | None = None    # default 1/sqrt(d_h + d_r) (reading R1)
+
+    @property
+    def scale(self) -> float:
+        return self.sm_scale if self.sm_scale is not None else 1.0 / math.sqrt(self.d_h + self.d_r)
+
+
+def make_config(spec: LayerSpec, k: int, g: int, rank: int) -> abi.tpla_config:
+    return abi.tpla_config(spec.h_q, spec.d_c, spec.d_r, spec.d_h, spec.D, k, g, rank, spec.eps, spec.scale)
+
+
+def bf16_from_bits(bits: np.ndarray, device) -> torch.Tensor:
+    """uint16 bf16 bit patterns (host) -> bf16 tensor on ``device`` (bitwise copy)."""
+    t = torch.from_numpy(np.ascontiguousarray(bits, dtype=np.uint16).view(np.int16))
+    return t.view(torch.bfloat16).to(device)
+
+
+def bits_from_bf16(t: torch.Tensor) -> np.ndarray:
+    return t.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class TplaRank:
+    """One device's share of a TPLA layer (plan, weights, cache, workspace)."""
+
+    def __init__(self, spec: LayerSpec, *, k: int, g: int, rank: int, batch: int, max_seq_len: int,
+                 page_size: int = 64, device="cuda", page_perm_seed: int | None = None, extra_pages: int = 0):
+        self.spec = spec
+        self.k, self.g, self.rank = k, g, rank
+        self.cfg = make_config(spec, k, g, rank)
+        self.plan = abi.tpla_make_plan(self.cfg)
+        self.device = torch.device(device)
+        self.batch = batch
+        self.max_seq_len = max_seq_len
+        self.page_size = page_size
+        self.max_pages = (max_seq_len + page_size - 1) // page_size
+        self.row_stride = ((self.plan.row_width + 63) // 64) * 64
+        num_pages = batch * self.max_pages + extra_pages
+        self.cache_buf = torch.zeros((num_pages, page_size, self.row_stride), dtype=torch.bfloat16, device=self.device)
+        order = np.arange(num_pages, dtype=np.int64)
+        if page_perm_seed is not None:      # scattered physical pages (exercises the page table)
+            order = np.random.default_rng(page_perm_seed).permutation(num_pages)
+        self.block_table_host = order[:batch * self.max_pages].reshape(batch, self.max_pages).astype(np.int32)
+        self.block_table = torch.from_numpy(self.block_table_host).to(self.device)
+        self.cache = abi.tpla_cache(self.cache_buf.data_ptr(), self.block_table.data_ptr(), num_pages, page_size,
+                                    self.max_pages, self.row_stride, batch)
+        self.ws_bytes = abi.tpla_decode_workspace_bytes(self.cfg, batch, max_seq_len)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.weights = None
+        self._wbufs = None
+
+    # ---- offline conversion
+    def convert(self, W_UK, W_UV, gamma, W_O, *, xform: int, sign_seed: int = 0, U_pca=None, alpha=None, mu=None):
+        """W_UK, W_UV [d_c, h_q d_h], gamma [d_c], W_O [h_q d_h, D]: host bf16 bits (uint16)."""
+        g = self.g
+        alpha = np.full(g, float(g)) if alpha is None else np.asarray(alpha, float)
+        mu = alpha.copy() if mu is None else np.asarray(mu, float)
+        nuk, nuv, nwo, nxf = abi.tpla_weights_bytes(self.cfg, xform)
+        dev = self.device
+        self._wbufs = (torch.empty(nuk // 2, dtype=torch.bfloat16, device=dev),
+                       torch.empty(nuv // 2, dtype=torch.bfloat16, device=dev),
+                       torch.empty(nwo // 2, dtype=torch.bfloat16, device=dev),
+                       torch.empty(max(nxf // 4, 1), dtype=torch.float32, device=dev))
+        w = abi.tpla_weights(self._wbufs[0].data_ptr(), self._wbufs[1].data_ptr(), self._wbufs[2].data_ptr(),
+                             self._wbufs[3].data_ptr() if nxf else None, xform, 0.0, 0.0)
+        abi.tpla_convert_weights(self.cfg, xform, sign_seed, U_pca, alpha, mu, W_UK, W_UV, gamma, W_O, w,
+                                 stream_ptr())
+        self.weights = w
+        return w
+
+    # ---- K1
+    def append(self, c_kv: torch.Tensor, k_pe: torch.Tensor, seq_idx: torch.Tensor, pos: torch.Tensor,
+               rms_mode: int = abi.RMS_SLICED, n_dropped: torch.Tensor | None = None, stream=None):
+        n = int(c_kv.shape[0])
+        abi.tpla_append_kv(self.cfg, self.weights, self.cache, c_kv, k_pe, seq_idx, pos, n, rms_mode, n_dropped,
+                           stream_ptr(stream))
+
+    def prefill(self, c_kv, k_pe, seq_idx, pos, stream=None):
+        n = int(c_kv.shape[0])
+        abi.tpla_prefill_mla(self.cfg, self.weights, self.cache, c_kv, k_pe, seq_idx, pos, n, None,
+                             stream_ptr(stream))
+
+    # ---- K2..K5 (+ C1)
+    def decode(self, q_nope, q_pe, seq_lens, y, out=None, *, B: int | None = None, accumulate=False, comm=None,
+               stream=None):
+        B = int(q_nope.shape[0]) if B is None else B
+        abi.tpla_decode(self.cfg, self.weights, self.cache, q_nope, q_pe, seq_lens, B, self.max_seq_len, self.ws,
+                        self.ws_bytes, y, out, abi.DECODE_ACCUMULATE if accumulate else 0, comm, stream_ptr(stream))
+
+    def decode_attention(self, q_lat, q_pe, seq_lens, O, lse=None, *, B: int | None = None, stream=None):
+        B = int(q_lat.shape[0]) if B is None else B
+        abi.tpla_decode_attention(self.cfg, self.cache, q_lat, q_pe, seq_lens, B, self.max_seq_len, self.ws,
+                                  self.ws_bytes, O, lse, stream_ptr(stream))
+
+    # ---- host view of the cache (tests)
+    def cache_rows_bits(self, b: int, n: int) -> np.ndarray:
+        """bf16 bits [n, row_stride] of sequence b's first n tokens, gathered through the page table."""
+        img = bits_from_bf16(self.cache_buf)
+        pages = self.block_table_host[b]
+        t = np.arange(n)
+        return img[pages[t // self.page_size], t % self.page_size]
+

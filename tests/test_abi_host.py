@@ -1,0 +1,148 @@
+"""Host-side checks of libtpla.so (no GPU): it loads, exports every symbol include/tpla.h
+declares, and its integer / host-only entry points match the oracle bit for bit."""
+import ctypes
+import itertools
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import numerics, plan as oplan, reparam
+import paper_2508_15881_b200 as pkg
+from paper_2508_15881_b200 import _abi as abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "tpla.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(tpla_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_symbols_exported():
+    syms = header_symbols()
+    assert len(syms) >= 15
+    out = subprocess.run(["nm", "-D", "--defined-only", abi.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (tpla_\w+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    for s in syms:                                   # and the binding wraps all of them
+        assert s in abi.EXPORTED
+        assert callable(getattr(abi, s))
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", abi.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_counter():
+    assert "sm_100a" in abi.tpla_version()
+    assert abi.tpla_launch_count() >= 0
+
+
+def cfg(h_q=128, d_c=512, d_r=64, d_h=128, D=7168, k=2, g=2, rank=0):
+    return abi.tpla_config(h_q, d_c, d_r, d_h, D, k, g, rank, 1e-6, 1.0 / np.sqrt(d_h + d_r))
+
+
+def test_make_plan_bit_exact_against_oracle():
+    n = 0
+    for (k, g), (h_q, d_c, d_r) in itertools.product(
+            [(1, 1), (2, 1), (2, 2), (4, 1), (4, 2), (4, 4), (8, 1), (8, 2), (8, 4), (8, 8)],
+            [(128, 512, 64), (64, 512, 64), (4, 64, 16), (6, 64, 16)]):
+        if h_q % (k // g):
+            continue
+        for r in range(k):
+            p = abi.tpla_make_plan(cfg(h_q, d_c, d_r, k=k, g=g, rank=r))
+            q = oplan.make_plan(k, g, h_q, d_c, d_r, r)
+            assert (p.rank, p.shard, p.head_block, p.head_begin, p.head_end, p.lat_begin, p.lat_end, p.row_width,
+                    p.h_loc, p.w_lat) == (q.rank, q.shard, q.head_block, q.head_begin, q.head_end, q.lat_begin,
+                                          q.lat_end, q.row_width, q.h_loc, q.w_lat)
+            n += 1
+    assert n > 100
+
+
+@pytest.mark.parametrize("bad,status", [
+    (dict(k=3, g=2), abi.ERR_DIVISIBILITY), (dict(k=4, g=3), abi.ERR_DIVISIBILITY),
+    (dict(h_q=6, k=4, g=1), abi.ERR_DIVISIBILITY), (dict(rank=2), abi.ERR_INVALID_ARG),
+    (dict(d_r=63), abi.ERR_SHAPE), (dict(d_c=0), abi.ERR_SHAPE)])
+def test_make_plan_rejects(bad, status):
+    with pytest.raises(abi.TplaError) as ei:
+        abi.tpla_make_plan(cfg(**bad))
+    assert ei.value.status == status
+    assert abi._lib.tpla_last_error().decode()
+
+
+@pytest.mark.parametrize("seed", [0, 1, 1234567, 2 ** 63 + 5])
+def test_hadamard_signs_bit_exact(seed):
+    assert np.array_equal(abi.tpla_hadamard_signs(seed, 512), numerics.sign_vector(seed, 512).astype(np.float32))
+
+
+def test_pca_alpha_golden():
+    a = abi.tpla_pca_alpha(np.array([4.0, 3.0, 2.0, 1.0]), 2)
+    assert np.allclose(a, [10 / 7, 10 / 3], rtol=1e-7)
+    lam = np.sort(np.random.default_rng(0).random(512))[::-1]
+    assert np.allclose(abi.tpla_pca_alpha(lam, 4), reparam.pca_alpha(lam, 4), rtol=1e-6)
+
+
+def test_weights_bytes():
+    c = cfg(k=4, g=2, rank=3)          # H_loc 64, W_lat 256
+    uk, uv, wo, xf = abi.tpla_weights_bytes(c, abi.XFORM_PCA)
+    assert uk == 64 * 256 * 128 * 2 and uv == uk
+    assert wo == 7168 * 64 * 128 * 2
+    assert xf == 512 * 256 * 4
+    assert abi.tpla_weights_bytes(c, abi.XFORM_HADAMARD)[3] == 512 * 4
+    assert abi.tpla_weights_bytes(c, abi.XFORM_IDENTITY)[3] == 0
+
+
+def test_workspace_bytes_monotone():
+    c = cfg()
+    a = abi.tpla_decode_workspace_bytes(c, 32, 32768)
+    b = abi.tpla_decode_workspace_bytes(c, 64, 32768)
+    assert 0 < a < b
+    with pytest.raises(abi.TplaError):
+        abi.tpla_decode_workspace_bytes(c, 0, 32768)
+
+
+def test_decode_rejects_before_launch():
+    # validation happens before any launch: NULL pointers -> INVALID_ARG, unsupported W_lat -> UNSUPPORTED
+    c = cfg(k=1, g=1)                  # W_lat 512: beyond this build's decode kernels
+    w = abi.tpla_weights(1 << 20, 1 << 20, 1 << 20, None, 0, 1.0, 1.0)
+    cache = abi.tpla_cache(1 << 20, 1 << 20, 16, 64, 4, 576, 2)
+    with pytest.raises(abi.TplaError) as ei:
+        abi.tpla_decode(c, w, cache, 1 << 20, 1 << 20, 1 << 20, 2, 256, 1 << 20, 1 << 30, 1 << 20)
+    assert ei.value.status == abi.ERR_UNSUPPORTED
+    c = cfg()
+    with pytest.raises(abi.TplaError) as ei:
+        abi.tpla_decode(c, w, cache, None, 1 << 20, 1 << 20, 2, 256, 1 << 20, 1 << 30, 1 << 20)
+    assert ei.value.status in (abi.ERR_INVALID_ARG, abi.ERR_SHAPE)
+    n_before = abi.tpla_launch_count()
+    cache_bad = abi.tpla_cache(1 << 20, 1 << 20, 16, 60, 4, 320, 2)   # page size not a multiple of 64
+    with pytest.raises(abi.TplaError) as ei:
+        abi.tpla_decode(c, w, cache_bad, 1 << 20, 1 << 20, 1 << 20, 2, 256, 1 << 20, 1 << 30, 1 << 20)
+    assert ei.value.status == abi.ERR_SHAPE
+    assert abi.tpla_launch_count() == n_before
+
+
+def test_prefill_attention_is_declared_unsupported():
+    c = cfg()
+    w = abi.tpla_weights(None, None, None, None, 0, 2.0, 2.0)
+    cache = abi.tpla_cache(1 << 20, 1 << 20, 16, 64, 4, 320, 2)
+    with pytest.raises(abi.TplaError) as ei:
+        abi.tpla_prefill_mla(c, w, cache, 1 << 20, 1 << 20, 1 << 20, 1 << 20, 4, 1 << 20)
+    assert ei.value.status == abi.ERR_UNSUPPORTED
+
+
+def test_import_fails_loudly_without_library(tmp_path):
+    # a copy of the package without libtpla.so must raise at import (no CPU fallback)
+    import shutil
+    import sys
+    dst = tmp_path / "paper_2508_15881_b200"
+    shutil.copytree(os.path.dirname(abi.__file__), dst, ignore=shutil.ignore_patterns("*.so", "build", "__pycache__"))
+    code = "from paper_2508_15881_b200 import abi"
+    r = subprocess.run([sys.executable, "-c", code], cwd=tmp_path, capture_output=True, text=True)
+    assert r.returncode != 0 and "libtpla.so" in r.stderr

@@ -1,0 +1,324 @@
+"""GPU parity: libtpla.so (through the C-ABI) against the fp64 oracle on the same seeded bf16 inputs.
+
+Tolerances: integer layout bit-exact; cache rows within 1 bf16 ulp;
+attention / end-to-end outputs per row ‖gpu − ref‖_∞ / ‖ref‖_∞ ≤ 1e-2 (reading R18, the
+north-star bound), also reported as relative L2.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import numerics, plan as oplan, reparam, tpla
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2508_15881_b200 import _abi as abi
+    from paper_2508_15881_b200.runtime import LayerSpec, TplaRank, bf16_from_bits, bits_from_bf16
+
+TOL = 1e-2
+
+
+def f64(b):
+    return numerics.bf16_to_f64(b)
+
+
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def row_rel_err(got, ref):
+    got = np.asarray(got, np.float64).reshape(ref.shape[0], -1)
+    ref = np.asarray(ref, np.float64).reshape(ref.shape[0], -1)
+    return np.max(np.max(np.abs(got - ref), axis=1) / np.max(np.abs(ref), axis=1))
+
+
+def spec_of(d: synth.ModelDims):
+    return LayerSpec(d.h_q, d.d_c, d.d_r, d.d_h, d.D)
+
+
+def transform_inputs(kind, dims, seed, g):
+    """(xform id, sign seed, U fp64, U_pca fp32 host or None, alpha[g])."""
+    if kind == "identity":
+        return abi.XFORM_IDENTITY, 0, np.eye(dims.d_c), None, np.full(g, float(g))
+    if kind == "hadamard":
+        return abi.XFORM_HADAMARD, seed, reparam.hadamard_U(dims.d_c, seed), None, np.full(g, float(g))
+    # PCA basis planted by the generator (population eigenvectors V, eigenvalues sigma^2)
+    V = synth.random_orthogonal(dims.d_c, seed)
+    lam = synth.latent_spectrum(dims.d_c, dims.n_outlier) ** 2
+    order = np.argsort(-lam, kind="stable")
+    U = V[:, order]
+    U32 = U.astype(np.float32)
+    return abi.XFORM_PCA, 0, U32.astype(np.float64), U32, abi.tpla_pca_alpha(lam[order], g).astype(np.float64)
+
+
+def upload_rows(rank, b, rows_bits):
+    """Write [S, W] bf16 rows of sequence b into the paged cache (test setup)."""
+    S, W = rows_bits.shape
+    img = torch.from_numpy(rows_bits.view(np.int16)).view(torch.bfloat16).to(rank.cache_buf.device)
+    for t0 in range(0, S, rank.page_size):
+        page = int(rank.block_table_host[b, t0 // rank.page_size])
+        n = min(rank.page_size, S - t0)
+        rank.cache_buf[page, :n, :W] = img[t0:t0 + n]
+
+
+# ----------------------------------------------------------------------------- K1 layout
+@pytest.mark.parametrize("dname", ["tiny", "dsv3"])
+def test_append_layout_bit_exact(dname):
+    """identity + RMS_NONE: the cache image is a byte copy of (c_j ‖ k_pe) at the paged address."""
+    d = dev()
+    dims = synth.PRESETS[dname]
+    k = g = 2
+    B, S = 3, 150
+    for rank_id in range(k):
+        r = TplaRank(spec_of(dims), k=k, g=g, rank=rank_id, batch=B, max_seq_len=256, device=d, page_perm_seed=7,
+                     extra_pages=3)
+        w = synth.gen_weights(dims, 1)
+        r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_IDENTITY)
+        rng = np.random.default_rng(3)
+        seq = np.repeat(np.arange(B), S).astype(np.int32)
+        pos = np.tile(np.arange(S), B).astype(np.int32)
+        perm = rng.permutation(seq.size)                     # arbitrary append order
+        ckv = np.concatenate([synth.gen_raw_ckv(dims, S, 5, b) for b in range(B)])
+        kpe = np.concatenate([synth.gen_kpe(dims, S, 5, b) for b in range(B)])
+        r.append(bf16_from_bits(ckv[perm], d), bf16_from_bits(kpe[perm], d),
+                 torch.from_numpy(seq[perm]).to(d), torch.from_numpy(pos[perm]).to(d), abi.RMS_NONE)
+        torch.cuda.synchronize()
+        pl = oplan.make_plan(k, g, dims.h_q, dims.d_c, dims.d_r, rank_id)
+        expect = np.zeros_like(bits_from_bf16(r.cache_buf))
+        for b in range(B):
+            for t in range(S):
+                page = r.block_table_host[b, t // r.page_size]
+                expect[page, t % r.page_size, :pl.w_lat] = ckv[b * S + t, pl.lat_begin:pl.lat_end]
+                expect[page, t % r.page_size, pl.w_lat:pl.row_width] = kpe[b * S + t]
+        assert np.array_equal(bits_from_bf16(r.cache_buf), expect)
+
+
+def test_append_drops_out_of_range():
+    d = dev()
+    dims = synth.PRESETS["tiny"]
+    r = TplaRank(spec_of(dims), k=2, g=2, rank=0, batch=2, max_seq_len=64, device=d)
+    w = synth.gen_weights(dims, 1)
+    r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_IDENTITY)
+    ckv = bf16_from_bits(synth.gen_raw_ckv(dims, 4, 1, 0), d)
+    kpe = bf16_from_bits(synth.gen_kpe(dims, 4, 1, 0), d)
+    seq = torch.tensor([0, 5, -1, 1], dtype=torch.int32, device=d)
+    pos = torch.tensor([0, 0, 0, 64], dtype=torch.int32, device=d)
+    nd = torch.zeros(1, dtype=torch.int32, device=d)
+    r.append(ckv, kpe, seq, pos, abi.RMS_SLICED, n_dropped=nd)
+    torch.cuda.synchronize()
+    assert int(nd.item()) == 3
+    img = bits_from_bf16(r.cache_buf)
+    assert np.count_nonzero(img) > 0 and np.count_nonzero(img[r.block_table_host[1]]) == 0
+
+
+# ----------------------------------------------------------------------------- K1 values
+@pytest.mark.parametrize("dname", ["tiny", "odd", "dsv3"])
+@pytest.mark.parametrize("kind", ["identity", "hadamard", "pca"])
+@pytest.mark.parametrize("mode", ["sliced", "exact"])
+@pytest.mark.parametrize("g", [2, 4])
+def test_append_rows_match_oracle(dname, kind, mode, g):
+    d = dev()
+    dims = synth.PRESETS[dname]
+    k = g
+    xf, seed, U, U32, alpha = transform_inputs(kind, dims, 11, g)
+    basis = U if kind == "pca" else None
+    n = 70
+    ckv = synth.gen_raw_ckv(dims, n, 9, 0, basis=basis)
+    kpe = synth.gen_kpe(dims, n, 9, 0)
+    w = synth.gen_weights(dims, 2)
+    for rank_id in range(k):
+        r = TplaRank(spec_of(dims), k=k, g=g, rank=rank_id, batch=1, max_seq_len=128, device=d)
+        r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=xf, sign_seed=seed, U_pca=U32, alpha=alpha)
+        mode_id = abi.RMS_SLICED if mode == "sliced" else abi.RMS_EXACT
+        r.append(bf16_from_bits(ckv, d), bf16_from_bits(kpe, d), torch.zeros(n, dtype=torch.int32, device=d),
+                 torch.arange(n, dtype=torch.int32, device=d), mode_id)
+        torch.cuda.synchronize()
+        pl = oplan.make_plan(k, g, dims.h_q, dims.d_c, dims.d_r, rank_id)
+        ref = tpla.cache_rows(f64(ckv), f64(kpe), U, pl, alpha[pl.shard], 1e-6, mode)
+        got = f64(r.cache_rows_bits(0, n)[:, :pl.row_width])
+        # within one bf16 ulp of the fp64 value (fp32 arithmetic on the GPU, RNE store)
+        ulp = np.abs(numerics.round_bf16(ref)) * 2.0 ** -7
+        assert np.all(np.abs(got - ref) <= ulp + 1e-30), np.max(np.abs(got - ref) / (ulp + 1e-30))
+
+
+# ----------------------------------------------------------------------------- K3+K4
+def attention_case(d, dims, g, B, S_list, seed=0, peak=1.0, needle=False, page_perm=None):
+    k = g
+    r = TplaRank(spec_of(dims), k=k, g=g, rank=g - 1, batch=B, max_seq_len=max(S_list), device=d,
+                 page_perm_seed=page_perm)
+    pl = oplan.make_plan(k, g, dims.h_q, dims.d_c, dims.d_r, g - 1)
+    rng = np.random.default_rng(seed)
+    rows = []
+    for b, S in enumerate(S_list):
+        rb = synth.bf16_bits(rng.standard_normal((S, pl.row_width)).astype(np.float32))
+        rows.append(rb)
+        upload_rows(r, b, rb)
+    q_lat = rng.standard_normal((B, pl.h_loc, pl.w_lat)).astype(np.float32) * peak
+    if needle:
+        q_lat *= 0.2
+    q_lat_b = synth.bf16_bits(q_lat)
+    qpe_b = synth.bf16_bits(rng.standard_normal((B, dims.h_q, dims.d_r)).astype(np.float32) * peak)
+    if needle:   # a few very large logits late in the sequence: exercises the running-max rescale
+        for b, S in enumerate(S_list):
+            t = S - 1 - rng.integers(0, max(1, S // 8))
+            rows[b][t, :pl.w_lat] = synth.bf16_bits(np.sign(f64(q_lat_b[b, 0])) * 4.0)
+            upload_rows(r, b, rows[b])
+    O = torch.zeros((B, pl.h_loc, pl.w_lat), dtype=torch.float32, device=d)
+    lse = torch.zeros((B, pl.h_loc), dtype=torch.float32, device=d)
+    r.decode_attention(bf16_from_bits(q_lat_b, d), bf16_from_bits(qpe_b, d),
+                       torch.tensor(S_list, dtype=torch.int32, device=d), O, lse)
+    torch.cuda.synchronize()
+    heads = slice(pl.head_begin, pl.head_end)
+    for b, S in enumerate(S_list):
+        Oref, lref, _, _ = tpla.shard_attention(f64(q_lat_b[b]), f64(qpe_b[b, heads]), f64(rows[b]), pl.w_lat,
+                                                 dims_scale(dims))
+        e = row_rel_err(O[b].cpu().numpy(), Oref)
+        assert e <= TOL, (b, S, e)
+        assert np.max(np.abs(lse[b].cpu().numpy() - lref)) < 1e-2 * max(1.0, np.max(np.abs(lref)))
+
+
+def dims_scale(dims):
+    return 1.0 / np.sqrt(dims.d_h + dims.d_r)
+
+
+@pytest.mark.parametrize("dname,g", [("tiny", 2), ("odd", 2), ("dsv3", 2), ("dsv3", 4), ("dsv3", 8), ("kimi", 4)])
+def test_attention_parity_small(dname, g):
+    d = dev()
+    attention_case(d, synth.PRESETS[dname], g, 3, [1, 77, 300], page_perm=3)
+
+
+def test_attention_parity_edge_lengths():
+    d = dev()
+    attention_case(d, synth.PRESETS["dsv3"], 2, 6, [1, 63, 64, 65, 128, 129], seed=1)
+    attention_case(d, synth.PRESETS["dsv3"], 2, 2, [4097, 2000], seed=2, needle=True)
+    attention_case(d, synth.PRESETS["dsv3"], 8, 2, [1500, 3], seed=4, peak=3.0)
+
+
+# ----------------------------------------------------------------------------- end to end (K1..K5)
+def e2e_case(d, dims, k, g, kind, S_list, *, seed=0, modes=("exact", "sliced"), check_rank_parts=True):
+    """All k ranks of a (k, g) plan run on this GPU, each accumulating into y (k-shard emulation);
+    compared with the oracle's full step (sum over ranks)."""
+    B = len(S_list)
+    xf, sseed, U, U32, alpha = transform_inputs(kind, dims, 21, g)
+    basis = U if kind == "pca" else None
+    w = synth.gen_weights(dims, seed + 1)
+    q, qpe = synth.gen_queries(dims, B, seed + 2)
+    # prompt rows (EXACT, PD-separated prefill P:421) then decode rows (SLICED) appended one by one
+    n_prompt = [max(1, S - 3) for S in S_list]
+    c_raw = [synth.gen_raw_ckv(dims, S, seed + 3, b, basis=basis) for b, S in enumerate(S_list)]
+    k_pe = [synth.gen_kpe(dims, S, seed + 3, b) for b, S in enumerate(S_list)]
+    y = torch.zeros((B, dims.D), dtype=torch.float32, device=d)
+    ranks = []
+    for rid in range(k):
+        r = TplaRank(spec_of(dims), k=k, g=g, rank=rid, batch=B, max_seq_len=max(S_list), device=d,
+                     page_perm_seed=rid)
+        r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=xf, sign_seed=sseed, U_pca=U32, alpha=alpha)
+        seq = np.concatenate([np.full(n, b, np.int32) for b, n in enumerate(n_prompt)])
+        pos = np.concatenate([np.arange(n, dtype=np.int32) for n in n_prompt])
+        ck = np.concatenate([c_raw[b][:n] for b, n in enumerate(n_prompt)])
+        kp = np.concatenate([k_pe[b][:n] for b, n in enumerate(n_prompt)])
+        r.prefill(bf16_from_bits(ck, d), bf16_from_bits(kp, d), torch.from_numpy(seq).to(d),
+                  torch.from_numpy(pos).to(d))
+        for step in range(3):
+            sel = [b for b, S in enumerate(S_list) if n_prompt[b] + step < S]
+            if not sel:
+                continue
+            ck = np.stack([c_raw[b][n_prompt[b] + step] for b in sel])
+            kp = np.stack([k_pe[b][n_prompt[b] + step] for b in sel])
+            r.append(bf16_from_bits(ck, d), bf16_from_bits(kp, d), torch.tensor(sel, dtype=torch.int32, device=d),
+                     torch.tensor([n_prompt[b] + step for b in sel], dtype=torch.int32, device=d), abi.RMS_SLICED)
+        r.decode(bf16_from_bits(q, d), bf16_from_bits(qpe, d), torch.tensor(S_list, dtype=torch.int32, device=d),
+                 y, accumulate=True)
+        ranks.append(r)
+    out = torch.empty((B, dims.D), dtype=torch.bfloat16, device=d)
+    abi.tpla_sync(0)
+    torch.cuda.synchronize()
+    pb = tpla.Problem(W_UK=f64(w.W_UK), W_UV=f64(w.W_UV), gamma=f64(w.gamma), W_O=f64(w.W_O), U=U,
+                      alpha=np.asarray(alpha, float), mu=np.asarray(alpha, float),
+                      c_raw=[f64(c) for c in c_raw], k_pe=[f64(x) for x in k_pe],
+                      modes=[[tpla.EXACT] * n + [tpla.SLICED] * (S - n) for S, n in zip(S_list, n_prompt)],
+                      q_nope=f64(q), q_pe=f64(qpe), h_q=dims.h_q, d_h=dims.d_h, eps=1e-6,
+                      sm_scale=dims_scale(dims))
+    ref = tpla.tpla_decode_step(pb, k, g)
+    got = y.cpu().numpy()
+    e = row_rel_err(got, ref)
+    l2 = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert e <= TOL, (e, l2)
+    return e, l2
+
+
+@pytest.mark.parametrize("dname", ["tiny", "odd"])
+@pytest.mark.parametrize("k,g", [(2, 2), (4, 2), (4, 4), (2, 1)])
+@pytest.mark.parametrize("kind", ["identity", "hadamard", "pca"])
+def test_e2e_parity_tiny(dname, k, g, kind):
+    dims = synth.PRESETS[dname]
+    if dims.h_q % (k // g) or (dims.d_c // g) % 32:
+        pytest.skip("shape outside the plan / kernels")
+    e2e_case(dev(), dims, k, g, kind, [1, 77, 130])
+
+
+@pytest.mark.parametrize("k,g,kind", [(2, 2, "hadamard"), (2, 2, "pca"), (4, 4, "hadamard"), (8, 8, "hadamard"),
+                                      (4, 2, "identity")])
+def test_e2e_parity_dsv3_shape(k, g, kind):
+    e2e_case(dev(), synth.PRESETS["dsv3"], k, g, kind, [5, 200, 333])
+
+
+def test_e2e_parity_kimi_shape():
+    e2e_case(dev(), synth.PRESETS["kimi"], 4, 4, "hadamard", [64, 129])
+
+
+def test_bf16_output_and_nccl_world1():
+    """tpla_decode with a 1-rank NCCL communicator (the C1 call path) and the bf16 output cast."""
+    d = dev()
+    dims = synth.PRESETS["tiny"]
+    r = TplaRank(spec_of(dims), k=1, g=1, rank=0, batch=2, max_seq_len=64, device=d)
+    w = synth.gen_weights(dims, 4)
+    r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_HADAMARD, sign_seed=3)
+    n = 40
+    ck = bf16_from_bits(np.concatenate([synth.gen_raw_ckv(dims, n, 1, b) for b in range(2)]), d)
+    kp = bf16_from_bits(np.concatenate([synth.gen_kpe(dims, n, 1, b) for b in range(2)]), d)
+    seq = torch.repeat_interleave(torch.arange(2, dtype=torch.int32), n).to(d)
+    pos = torch.arange(n, dtype=torch.int32).repeat(2).to(d)
+    r.append(ck, kp, seq, pos, abi.RMS_SLICED)
+    q, qpe = synth.gen_queries(dims, 2, 5)
+    lens = torch.tensor([n, n - 7], dtype=torch.int32, device=d)
+    y0 = torch.zeros((2, dims.D), dtype=torch.float32, device=d)
+    r.decode(bf16_from_bits(q, d), bf16_from_bits(qpe, d), lens, y0)
+    comm = abi.tpla_comm_init(abi.tpla_comm_unique_id(), 1, 0)
+    y1 = torch.zeros_like(y0)
+    out = torch.empty((2, dims.D), dtype=torch.bfloat16, device=d)
+    r.decode(bf16_from_bits(q, d), bf16_from_bits(qpe, d), lens, y1, out, comm=comm)
+    torch.cuda.synchronize()
+    abi.tpla_comm_destroy(comm)
+    assert torch.equal(y0, y1)
+    assert torch.equal(out, y1.to(torch.bfloat16))
+
+
+def test_full_size_sampled_attention_c1():
+    """configs[1] shard at full size (B=32, S=32K, H_loc=128, W=320) in the bench's launch
+    configuration; two sampled sequences checked against the oracle."""
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    g, B, S = 2, 32, 32768
+    r = TplaRank(spec_of(dims), k=2, g=2, rank=1, batch=B, max_seq_len=S, device=d)
+    pl = oplan.make_plan(2, 2, dims.h_q, dims.d_c, dims.d_r, 1)
+    gen = torch.Generator(device=d)
+    gen.manual_seed(123)
+    r.cache_buf[..., :pl.row_width].normal_(generator=gen)
+    q_lat = torch.randn((B, pl.h_loc, pl.w_lat), generator=gen, device=d).to(torch.bfloat16)
+    qpe = torch.randn((B, dims.h_q, dims.d_r), generator=gen, device=d).to(torch.bfloat16)
+    lens = torch.full((B,), S, dtype=torch.int32, device=d)
+    lens[5] = S - 1000
+    O = torch.zeros((B, pl.h_loc, pl.w_lat), dtype=torch.float32, device=d)
+    r.decode_attention(q_lat, qpe, lens, O)
+    torch.cuda.synchronize()
+    for b in (5, 31):
+        n = int(lens[b])
+        rows = f64(r.cache_rows_bits(b, n)[:, :pl.row_width])
+        Oref, _, _, _ = tpla.shard_attention(f64(bits_from_bf16(q_lat[b])), f64(bits_from_bf16(qpe[b])), rows,
+                                              pl.w_lat, dims_scale(dims))
+        assert row_rel_err(O[b].cpu().numpy(), Oref) <= TOL
