@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
+    p.add_argument("--profile-region", action="store_true",
+                   help="cudaProfilerStart/Stop around the timed region (for ncu --profile-from-start off)")
     return p.parse_args()
 
 
@@ -358,12 +360,16 @@ def main():
     torch.cuda.synchronize()
     n0 = abi.tpla_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if args.profile_region:
+        torch.cuda.cudart().cudaProfilerStart()
     with ClockSampler(local) as clocks:
         ev0.record(stream)
         for i in range(args.steps):
             step(i)
         ev1.record(stream)
         torch.cuda.synchronize()
+    if args.profile_region:
+        torch.cuda.cudart().cudaProfilerStop()
     barrier()
     launches = abi.tpla_launch_count() - n0
     abi.tpla_profile_enable(False)

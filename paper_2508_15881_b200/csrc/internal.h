@@ -46,8 +46,10 @@ struct WsLayout {
   size_t o_lat;     // bf16 [B, H_loc, W_lat]   (combined O_j)
   size_t v;         // bf16 [B, H_loc*d_h]
   size_t y_part;    // fp32 [kslices, B, D]
+  size_t meta;      // int32 [B, 2] (persistent K3: first segment id, count)
   size_t total;
   int kslices;
+  int n_cta;        // persistent K3 grid
 };
 
 SplitPlan choose_split(int B, int max_seq_len);
@@ -70,6 +72,15 @@ cudaError_t launch_decode_attn(const Geom& g, const tpla_cache& cache, const uin
 
 cudaError_t launch_combine(const Geom& g, int B, const SplitPlan& sp, const float* o_part, const float* ml_part,
                            uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s);
+
+// Blackwell-native K3 (tcgen05/TMEM/TMA, persistent) and its segment combine.
+bool tc_attention_supported(const Geom& g, int B);
+int tc_num_ctas(int B, int max_seq_len);
+cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
+                                  const int32_t* seq_lens, int B, int n_cta, float* o_part, float* ml_part,
+                                  int32_t* meta, cudaStream_t s);
+cudaError_t launch_combine_seg(const Geom& g, int B, const float* o_part, const float* ml_part, const int32_t* meta,
+                               uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s);
 
 // y_part[ks, b, n] = sum_{k in slice ks} Wt[n, k] * v[b, k]; Wt [N, K] bf16, v [B, K] bf16.
 cudaError_t launch_skinny_gemm(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, int kslices,

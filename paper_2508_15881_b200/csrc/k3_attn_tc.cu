@@ -1,0 +1,469 @@
+// K3 (v1, Blackwell-native) — persistent split-K flash decoding of one TPLA shard on the
+// 5th-generation tensor cores, and its K4 combine.
+//
+// What it computes (Eq. tpla_softmax_one_device; RoPE part P:238-242):
+//   s_t = [Q'_j ‖ q^PE] · [ĉ_{j,t} ‖ k^PE_t]          (μ_j already folded into Q'_j)
+//   p_t = softmax over this shard's own tokens (sm_scale applied; no cross-device max/sum)
+//   O_j = Σ_t p_t ĉ_{j,t}
+//
+// Mapping: heads are the MMA M dimension (128 TMEM lanes, one head per lane).
+// Per 64-token tile:
+//   QK  S[128 x 64]   = Q'_j (TMEM, A operand, K = W_lat)  x  ĉ tileᵀ (smem, K-major)     tcgen05 TS
+//                     + q^PE (smem, A, K = 64)             x  k^PE tileᵀ (smem, K-major)   tcgen05 SS
+//   softmax on 4 warps (thread = head row), exp2 with a lazily-raised running max (the O
+//   accumulator is rescaled only when the max grows by more than 2^8), P written back to
+//   TMEM as bf16 over its own S columns
+//   PV  O[128 x W_lat] += P (TMEM, A, K = 64 tokens)       x  ĉ tile (smem, MN-major)      tcgen05 TS
+// The cache tile [64 tokens x (W_lat + 64)] arrives by TMA (SWIZZLE_128B, 64-column boxes)
+// into a 5-8 stage mbarrier ring; the same smem bytes serve as the K-major B operand of QK
+// and the MN-major B operand of PV, so every cache byte crosses HBM -> SMEM once.
+//
+// Work split: persistent grid (<= #SMs CTAs).  The flattened (sequence, 64-token tile) list is
+// cut into equal contiguous ranges, one per CTA; a range is a few segments (one per sequence
+// it touches).  Each segment leaves an unnormalised partial (O, m, l); K4 merges a sequence's
+// segments, whose ids are contiguous.
+//
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w3 schedule, w4-w7 softmax + Q loader + epilogue (warp w owns TMEM lanes 32*(w%4)..).
+#include <cuda.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace tpla {
+namespace {
+
+using namespace sm100;
+
+constexpr int kTile = 64;         // tokens per tile
+constexpr int kThreads = 256;
+constexpr int kMaxB = 512;        // sequences per launch supported by the smem schedule
+constexpr float kRescaleThreshold = 8.0f;   // log2 units: p <= 2^8 between max updates
+
+struct TcArgs {
+  const uint16_t* q_lat;       // [B, H_loc, W_lat]
+  const uint16_t* q_pe;        // [B, h_q, d_r]
+  const int32_t* block_table;  // [B, max_pages]
+  const int32_t* seq_lens;     // [B]
+  float* o_part;               // [max_segs, H_loc, W_lat]
+  float* ml_part;              // [max_segs, H_loc, 2]
+  int32_t* meta;               // [B, 2]: first segment id, segment count
+  int B, h_loc, h_q, head_begin, page_size, max_pages;
+  int cap;                     // max_pages * page_size: lengths beyond the page table are clamped
+  float scale_log2;
+};
+
+template <int W_LAT>
+struct Cfg {
+  static constexpr int W = W_LAT + 64;
+  static constexpr int NBOX = W / 64;                 // 64-column TMA boxes per tile
+  static constexpr int BOX_BYTES = kTile * 128;       // 8 KB
+  static constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
+  static constexpr int QPE_BYTES = 128 * 128;         // q^PE A operand [128 rows x 64] bf16
+  static constexpr int NST = std::min(8, (220 * 1024 - QPE_BYTES) / STAGE_BYTES);
+  static constexpr int SMEM = 1024 + QPE_BYTES + NST * STAGE_BYTES;
+  // TMEM columns
+  static constexpr int O_COL = 0;
+  static constexpr int Q_COL = W_LAT;                 // W_lat/2 columns of packed bf16
+  static constexpr int S_COL0 = (W_LAT + W_LAT / 2 + 63) / 64 * 64;
+  static constexpr int S_COLS = S_COL0 + 2 * kTile;
+  static constexpr int TMEM_COLS = S_COLS <= 256 ? 256 : 512;
+  static_assert(S_COLS <= 512, "TMEM budget");
+};
+
+struct Sched {
+  int lo, hi;          // tile range [lo, hi) in the flattened list
+  int b_first, b_last;
+  int seg_base;
+};
+
+__device__ __forceinline__ int upper_bound_cum(const int* cum, int n, int x) {  // first i with cum[i] > x
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (cum[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <int W_LAT>
+__global__ void __launch_bounds__(kThreads, 1)
+attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
+  using C = Cfg<W_LAT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* s_qpe = smem;
+  uint8_t* s_kv = smem + C::QPE_BYTES;
+  __shared__ uint64_t kv_full[C::NST], kv_empty[C::NST];
+  __shared__ uint64_t s_full[2], p_full[2], pv_done[2], q_ready;
+  __shared__ uint32_t tmem_base;
+  __shared__ int cum[kMaxB + 1];
+  __shared__ Sched sch;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c = blockIdx.x, n_cta = gridDim.x;
+
+  // ---------------------------------------------------------------- setup
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap);
+    for (int i = 0; i < C::NST; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 128); mbar_init(&pv_done[i], 1); }
+    mbar_init(&q_ready, 128);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
+  if (warp == 3) {
+    // tiles per sequence -> exclusive prefix sum (warp scan, 32 sequences per step)
+    int carry = 0;
+    for (int b0 = 0; b0 < a.B; b0 += 32) {
+      int b = b0 + lane;
+      int t = b < a.B ? (min(a.seq_lens[b], a.cap) + kTile - 1) / kTile : 0;
+      int x = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (b < a.B) cum[b] = carry + x - t;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) cum[a.B] = carry;
+    __syncwarp();
+    const long T = carry;
+    // segments of CTAs c' < c (each CTA range touches b_last - b_first + 1 sequences)
+    int before = 0;
+    for (int cc = lane; cc < c; cc += 32) {
+      int lo = int(cc * T / n_cta), hi = int((cc + 1) * T / n_cta);
+      if (lo < hi) before += upper_bound_cum(cum, a.B + 1, hi - 1) - upper_bound_cum(cum, a.B + 1, lo) + 1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+    if (lane == 0) {
+      sch.lo = int(c * T / n_cta);
+      sch.hi = int((c + 1) * T / n_cta);
+      sch.b_first = sch.lo < sch.hi ? upper_bound_cum(cum, a.B + 1, sch.lo) - 1 : 0;
+      sch.b_last = sch.lo < sch.hi ? upper_bound_cum(cum, a.B + 1, sch.hi - 1) - 1 : -1;
+      sch.seg_base = before;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tmem_base;
+  const Sched S = sch;
+
+  if (warp == 0) {
+    // ============================================================ TMA producer
+    if (lane == 0) {
+      int g = 0;
+      for (int b = S.b_first; b <= S.b_last; ++b) {
+        const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
+        for (int t = t0; t < t1; ++t, ++g) {
+          const int st = g % C::NST;
+          mbar_wait(&kv_empty[st], ((g / C::NST) & 1) ^ 1);
+          const int tok = (t - cum[b]) * kTile;
+          const int page = a.block_table[(long)b * a.max_pages + tok / a.page_size];
+          const int row = page * a.page_size + tok % a.page_size;
+          uint8_t* dst = s_kv + st * C::STAGE_BYTES;
+          mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
+#pragma unroll
+          for (int j = 0; j < C::NBOX; ++j) tma_load_2d(dst + j * C::BOX_BYTES, &tmap, j * 64, row, &kv_full[st], kEvictFirst);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================================================ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id_qk = idesc_bf16(128, kTile, false, false);
+      constexpr uint32_t id_pv = idesc_bf16(128, W_LAT, false, true);
+      const uint32_t qpe_addr = smem_addr(s_qpe);
+      int g = 0, seg = 0;
+      auto issue_pv = [&](int gp, bool first_pv) {
+        const int st = gp % C::NST;
+        mbar_wait(&p_full[gp & 1], (gp >> 1) & 1);
+        tc_fence_after();
+        const uint32_t kv = smem_addr(s_kv + st * C::STAGE_BYTES);
+        const uint32_t p_tmem = tb + C::S_COL0 + (gp & 1) * kTile;
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk)
+          mma_ts(tb + C::O_COL, p_tmem + kk * 8, desc_mnmajor_sw128(kv + kk * 2048, C::BOX_BYTES), id_pv,
+                 (first_pv && kk == 0) ? 0u : 1u);
+        mma_commit(&kv_empty[st]);
+        mma_commit(&pv_done[gp & 1]);
+      };
+      for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
+        const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
+        mbar_wait(&q_ready, seg & 1);
+        tc_fence_after();
+        for (int t = t0; t < t1; ++t, ++g) {
+          const int st = g % C::NST;
+          mbar_wait(&kv_full[st], (g / C::NST) & 1);
+          tc_fence_after();
+          const uint32_t kv = smem_addr(s_kv + st * C::STAGE_BYTES);
+          const uint32_t s_tmem = tb + C::S_COL0 + (g & 1) * kTile;
+#pragma unroll
+          for (int kk = 0; kk < W_LAT / 16; ++kk)     // Q'_j (TMEM) x ĉ tileᵀ
+            mma_ts(s_tmem, tb + C::Q_COL + kk * 8, desc_kmajor_sw128(kv + (kk >> 2) * C::BOX_BYTES + (kk & 3) * 32),
+                   id_qk, kk > 0 ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)              // q^PE (smem) x k^PE tileᵀ
+            mma_ss(s_tmem, desc_kmajor_sw128(qpe_addr + kk * 32),
+                   desc_kmajor_sw128(kv + (C::NBOX - 1) * C::BOX_BYTES + kk * 32), id_qk, 1u);
+          mma_commit(&s_full[g & 1]);
+          if (t > t0) issue_pv(g - 1, t - 1 == t0);
+        }
+        issue_pv(g - 1, t1 - 1 == t0);
+      }
+    }
+  } else if (warp >= 4) {
+    // ============================================================ softmax / Q loader / epilogue
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;                       // head row = TMEM lane
+    const uint32_t lane_base = tb + (uint32_t(q4 * 32) << 16);
+    const bool row_ok = r < a.h_loc;
+    int g = 0, seg = 0;
+    for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
+      const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
+      const int S_b = min(a.seq_lens[b], a.cap);
+      // ---- Q'_j row -> TMEM (A operand, bf16 pairs per 32-bit column); q^PE row -> swizzled smem
+      {
+        const uint4* src = reinterpret_cast<const uint4*>(a.q_lat + ((long)b * a.h_loc + r) * W_LAT);
+#pragma unroll
+        for (int c0 = 0; c0 < W_LAT / 2; c0 += 32) {
+          uint32_t w[32];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            uint4 u = row_ok ? src[c0 / 4 + v] : make_uint4(0, 0, 0, 0);
+            w[4 * v] = u.x; w[4 * v + 1] = u.y; w[4 * v + 2] = u.z; w[4 * v + 3] = u.w;
+          }
+          tmem_st32(lane_base + C::Q_COL + c0, w);
+        }
+        const uint4* pe = reinterpret_cast<const uint4*>(a.q_pe + ((long)b * a.h_q + a.head_begin + r) * 64);
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint4 u = row_ok ? pe[ch] : make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(s_qpe + r * 128 + ((ch ^ (r & 7)) << 4)) = u;
+        }
+        fence_proxy_async_smem();
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&q_ready);
+      }
+      float m_used = -INFINITY, l = 0.f;
+      for (int t = t0; t < t1; ++t, ++g) {
+        const int sb = g & 1;
+        mbar_wait(&s_full[sb], (g >> 1) & 1);
+        tc_fence_after();
+        uint32_t sv[64];
+        tmem_ld32(lane_base + C::S_COL0 + sb * kTile, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+        tmem_ld32(lane_base + C::S_COL0 + sb * kTile + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
+        tmem_ld_wait();
+        const int tok0 = (t - cum[b]) * kTile;
+        const int nvalid = min(kTile, S_b - tok0);
+        float* x = reinterpret_cast<float*>(sv);
+        float mx = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+          x[j] = j < nvalid ? x[j] * a.scale_log2 : -INFINITY;
+          mx = fmaxf(mx, x[j]);
+        }
+        if (mx > m_used + kRescaleThreshold) {
+          const float m_new = mx;
+          if (t > t0) {
+            // O holds PV(g-1) and earlier: wait for it, then scale the row in TMEM
+            const float f = ex2(m_used - m_new);
+            mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c0 = 0; c0 < W_LAT; c0 += 32) {
+              uint32_t ov[32];
+              tmem_ld32(lane_base + C::O_COL + c0, ov);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * f);
+              tmem_st32(lane_base + C::O_COL + c0, ov);
+            }
+            l *= f;
+          }
+          m_used = m_new;
+        }
+        uint32_t pw[32];
+        float ls = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float p0 = ex2(x[2 * j] - m_used), p1 = ex2(x[2 * j + 1] - m_used);
+          ls += p0 + p1;
+          pw[j] = pack_bf16(p0, p1);
+        }
+        l += ls;
+        tmem_st32(lane_base + C::S_COL0 + sb * kTile, pw);    // P over the first 32 columns of S(g)
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[sb]);
+      }
+      // ---- epilogue of the segment: unnormalised partial (O, m, l)
+      mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+      tc_fence_after();
+      const int seg_id = S.seg_base + seg;
+      {
+        float* op = a.o_part + ((long)seg_id * a.h_loc + r) * W_LAT;
+#pragma unroll 1
+        for (int c0 = 0; c0 < W_LAT; c0 += 32) {
+          uint32_t ov[32];
+          tmem_ld32(lane_base + C::O_COL + c0, ov);     // whole warp (.sync.aligned)
+          tmem_ld_wait();
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(op + c0 + j) = make_float4(__uint_as_float(ov[j]), __uint_as_float(ov[j + 1]),
+                                                                    __uint_as_float(ov[j + 2]), __uint_as_float(ov[j + 3]));
+          }
+        }
+        if (row_ok) {
+          a.ml_part[((long)seg_id * a.h_loc + r) * 2] = m_used;
+          a.ml_part[((long)seg_id * a.h_loc + r) * 2 + 1] = l;
+        }
+      }
+      // publish the sequence's segment range for K4: the CTA holding its first tile writes the
+      // first segment id, the CTA holding its last tile the last one (ids are contiguous)
+      if (r == 0 && t0 == cum[b]) a.meta[2 * b] = seg_id;
+      if (r == 0 && t1 == cum[b + 1]) a.meta[2 * b + 1] = seg_id;
+      tc_fence_before();
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tb);
+}
+
+// K4 for the persistent kernel: O = Σ_s 2^{m_s - M} O_s / Σ_s 2^{m_s - M} l_s over the
+// contiguous segment range of sequence b
+__global__ void combine_seg_kernel(const float* __restrict__ o_part, const float* __restrict__ ml_part,
+                                   const int32_t* __restrict__ meta, int h_loc, int w_lat,
+                                   uint16_t* __restrict__ o_bf16, float* __restrict__ o_f32, float* __restrict__ lse) {
+  const int h = blockIdx.x, b = blockIdx.y;
+  const int s0 = meta[2 * b], ns = meta[2 * b + 1] - s0 + 1;
+  float M = -INFINITY;
+  for (int s = 0; s < ns; ++s) M = fmaxf(M, ml_part[((long)(s0 + s) * h_loc + h) * 2]);
+  float L = 0.f;
+  for (int s = 0; s < ns; ++s) {
+    const float* ml = ml_part + ((long)(s0 + s) * h_loc + h) * 2;
+    L += exp2f(ml[0] - M) * ml[1];
+  }
+  const float inv = 1.f / L;
+  for (int col = threadIdx.x * 4; col < w_lat; col += blockDim.x * 4) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < ns; ++s) {
+      const float w = exp2f(ml_part[((long)(s0 + s) * h_loc + h) * 2] - M);
+      float4 v = *reinterpret_cast<const float4*>(o_part + ((long)(s0 + s) * h_loc + h) * w_lat + col);
+      acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
+    }
+    acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
+    const long off = ((long)b * h_loc + h) * w_lat + col;
+    if (o_f32) *reinterpret_cast<float4*>(o_f32 + off) = acc;
+    if (o_bf16) {
+      uint2 u;
+      u.x = pack_bf16(acc.x, acc.y);
+      u.y = pack_bf16(acc.z, acc.w);
+      *reinterpret_cast<uint2*>(o_bf16 + off) = u;
+    }
+  }
+  if (lse && threadIdx.x == 0) lse[(long)b * h_loc + h] = (M + log2f(L)) * 0.69314718055994531f;
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int W_LAT>
+cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaStream_t s) {
+  using C = Cfg<W_LAT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<W_LAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  KernelScope ks("K3_attn_tc", s);
+  attn_tc_kernel<W_LAT><<<n_cta, kThreads, C::SMEM, s>>>(map, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool tc_attention_supported(const Geom& g, int B) {
+  return g.d_r == 64 && (g.w_lat == 64 || g.w_lat == 128 || g.w_lat == 256) && g.h_loc <= 128 && B <= kMaxB;
+}
+
+int tc_num_ctas(int B, int max_seq_len) {
+  long tiles = (long)B * ((max_seq_len + kTile - 1) / kTile);
+  return int(std::max(1L, std::min<long>(num_sms(), tiles)));
+}
+
+cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
+                                  const int32_t* seq_lens, int B, int n_cta, float* o_part, float* ml_part,
+                                  int32_t* meta, cudaStream_t s) {
+  EncodeFn enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {cuuint64_t(cache.row_stride), cuuint64_t(cache.num_pages) * cache.page_size};
+  cuuint64_t strides[1] = {cuuint64_t(cache.row_stride) * 2};
+  cuuint32_t box[2] = {64, kTile};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, cache.base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  TcArgs a;
+  a.q_lat = q_lat; a.q_pe = q_pe; a.block_table = cache.block_table; a.seq_lens = seq_lens;
+  a.o_part = o_part; a.ml_part = ml_part; a.meta = meta;
+  a.B = B; a.h_loc = g.h_loc; a.h_q = g.h_q; a.head_begin = g.head_begin; a.page_size = cache.page_size;
+  a.max_pages = cache.max_pages_per_seq; a.scale_log2 = g.sm_scale * 1.4426950408889634f;
+  a.cap = cache.max_pages_per_seq * cache.page_size;
+  switch (g.w_lat) {
+    case 64: return launch_tc<64>(map, a, n_cta, s);
+    case 128: return launch_tc<128>(map, a, n_cta, s);
+    case 256: return launch_tc<256>(map, a, n_cta, s);
+  }
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_combine_seg(const Geom& g, int B, const float* o_part, const float* ml_part, const int32_t* meta,
+                               uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s) {
+  dim3 grid(g.h_loc, B);
+  int threads = std::min(64, std::max(32, g.w_lat / 4));
+  KernelScope ks("K4_combine", s);
+  combine_seg_kernel<<<grid, threads, 0, s>>>(o_part, ml_part, meta, g.h_loc, g.w_lat, o_bf16, o_f32, lse);
+  return cudaGetLastError();
+}
+
+}  // namespace tpla

@@ -207,15 +207,41 @@ WsLayout ws_layout(const Geom& g, int B, int max_seq_len) {
   L.kslices = std::max(1, std::min(K / 64, 16));
   while (L.kslices > 1 && (K / 64) % L.kslices) --L.kslices;
   if (K % (64 * L.kslices)) L.kslices = 1;
+  // partial (O, m, l) slots: B*n_split for the fixed split (mma.sync K3), n_cta + B segments
+  // for the persistent tcgen05 K3 (each CTA range touches at most one more sequence than it starts in)
+  L.n_cta = tc_num_ctas(B, max_seq_len);
+  const size_t parts = std::max(size_t(B) * sp.n_split, size_t(L.n_cta) + B);
   size_t off = 0;
   L.q_lat = off;   off += align256(size_t(B) * g.h_loc * g.w_lat * 2);
-  L.o_part = off;  off += align256(size_t(B) * sp.n_split * g.h_loc * g.w_lat * 4);
-  L.ml_part = off; off += align256(size_t(B) * sp.n_split * g.h_loc * 2 * 4);
+  L.o_part = off;  off += align256(parts * g.h_loc * g.w_lat * 4);
+  L.ml_part = off; off += align256(parts * g.h_loc * 2 * 4);
   L.o_lat = off;   off += align256(size_t(B) * g.h_loc * g.w_lat * 2);
   L.v = off;       off += align256(size_t(B) * K * 2);
   L.y_part = off;  off += align256(size_t(L.kslices) * B * g.D * 4);
+  L.meta = off;    off += align256(size_t(B) * 2 * 4);
   L.total = off;
   return L;
+}
+
+// K3 + K4: the tcgen05 kernel where its shapes allow (TPLA_ATTN=mma forces the legacy path)
+static cudaError_t run_attention(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
+                                 const int32_t* seq_lens, int B, int max_seq_len, const WsLayout& L, char* base,
+                                 uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s) {
+  auto* o_part = reinterpret_cast<float*>(base + L.o_part);
+  auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
+  const char* force = getenv("TPLA_ATTN");
+  const bool use_tc = tc_attention_supported(g, B) && !(force && strcmp(force, "mma") == 0);
+  cudaError_t e;
+  if (use_tc) {
+    auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
+    e = launch_decode_attn_tc(g, cache, q_lat, q_pe, seq_lens, B, L.n_cta, o_part, ml_part, meta, s);
+    if (e != cudaSuccess) return e;
+    return launch_combine_seg(g, B, o_part, ml_part, meta, o_bf16, o_f32, lse, s);
+  }
+  SplitPlan sp = choose_split(B, max_seq_len);
+  e = launch_decode_attn(g, cache, q_lat, q_pe, seq_lens, B, sp, o_part, ml_part, s);
+  if (e != cudaSuccess) return e;
+  return launch_combine(g, B, sp, o_part, ml_part, o_bf16, o_f32, lse, s);
 }
 
 }  // namespace tpla
@@ -456,12 +482,9 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
     return fail(TPLA_ERR_INVALID_ARG, "communicator world %d does not divide k=%d", comm->world, g.k);
   WsLayout L = ws_layout(g, B, max_seq_len);
   if (ws_bytes < L.total) return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, L.total);
-  SplitPlan sp = choose_split(B, max_seq_len);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(ws);
   auto* q_lat = reinterpret_cast<uint16_t*>(base + L.q_lat);
-  auto* o_part = reinterpret_cast<float*>(base + L.o_part);
-  auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
   auto* o_lat = reinterpret_cast<uint16_t*>(base + L.o_lat);
   auto* v = reinterpret_cast<uint16_t*>(base + L.v);
   auto* y_part = reinterpret_cast<float*>(base + L.y_part);
@@ -471,12 +494,10 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
   e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK), qn + size_t(g.head_begin) * g.d_h,
                        long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h, B, q_lat, s);
   if (e != cudaSuccess) return cuda_fail(e, "K2 absorb_q");
-  // K3: per-shard split-K flash decoding (Eq. tpla_softmax_one_device)
-  e = launch_decode_attn(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, sp, o_part, ml_part, s);
-  if (e != cudaSuccess) return cuda_fail(e, "K3 decode_attn");
-  // K4: combine the splits -> O_j
-  e = launch_combine(g, B, sp, o_part, ml_part, o_lat, nullptr, nullptr, s);
-  if (e != cudaSuccess) return cuda_fail(e, "K4 combine");
+  // K3 + K4: per-shard split-K flash decoding (Eq. tpla_softmax_one_device) -> O_j
+  e = run_attention(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, max_seq_len, L, base, o_lat,
+                    nullptr, nullptr, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K3/K4 decode attention");
   // K5a: v[b,h,:] = W^UV'_j[h]^T-applied O_j  (W^VO factored)
   e = launch_head_gemv("K5_W_UV", static_cast<const uint16_t*>(w->W_UV), o_lat, long(g.h_loc) * g.w_lat, g.h_loc, g.d_h,
                        g.w_lat, B, v, s);
@@ -510,16 +531,11 @@ tpla_status tpla_decode_attention(const tpla_config* cfg, const tpla_cache* cach
   if (!aligned16(q_lat) || !aligned16(ws)) return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
   WsLayout L = ws_layout(g, B, max_seq_len);
   if (ws_bytes < L.total) return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, L.total);
-  SplitPlan sp = choose_split(B, max_seq_len);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(ws);
-  auto* o_part = reinterpret_cast<float*>(base + L.o_part);
-  auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
-  cudaError_t e = launch_decode_attn(g, *cache, static_cast<const uint16_t*>(q_lat),
-                                     static_cast<const uint16_t*>(q_pe), seq_lens, B, sp, o_part, ml_part, s);
-  if (e != cudaSuccess) return cuda_fail(e, "K3 decode_attn");
-  e = launch_combine(g, B, sp, o_part, ml_part, nullptr, O, lse, s);
-  if (e != cudaSuccess) return cuda_fail(e, "K4 combine");
+  cudaError_t e = run_attention(g, *cache, static_cast<const uint16_t*>(q_lat), static_cast<const uint16_t*>(q_pe),
+                                seq_lens, B, max_seq_len, L, base, nullptr, O, lse, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K3/K4 decode attention");
   return ok();
 }
 
