@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
+    p.add_argument("--batch", type=int, default=None, help="override the workload batch (sweep)")
+    p.add_argument("--seq-len", type=int, default=None, help="override the workload context length (sweep)")
     p.add_argument("--profile-region", action="store_true",
                    help="cudaProfilerStart/Stop around the timed region (for ncu --profile-from-start off)")
     return p.parse_args()
@@ -270,7 +272,11 @@ def main():
     from paper_2508_15881_b200 import abi
     from paper_2508_15881_b200.runtime import LayerSpec, TplaRank, bf16_from_bits
 
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.batch:
+        wl["B"] = args.batch
+    if args.seq_len:
+        wl["S"] = args.seq_len
     N = args.gpus
     world = int(os.environ.get("WORLD_SIZE", "1"))
     proc = int(os.environ.get("RANK", "0"))

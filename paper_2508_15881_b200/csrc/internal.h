@@ -21,6 +21,7 @@ struct KernelScope {
   ~KernelScope();
   int slot = -1;
   cudaStream_t stream;
+  const char* name_;
 };
 
 // Resolved per-device problem geometry (validated).

@@ -271,11 +271,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           x[j] = j < nvalid ? x[j] * a.scale_log2 : -INFINITY;
           mx = fmaxf(mx, x[j]);
         }
-        if (mx > m_used + kRescaleThreshold) {
-          const float m_new = mx;
+        // Raise the running max only when it grew by more than 2^8 (p stays <= 256 in between).
+        // The decision is per row, but the TMEM loads/stores of a rescale are warp-collective
+        // (.sync.aligned), so the whole warp enters together; rows that keep their max scale by 1.
+        const bool need = mx > m_used + kRescaleThreshold;
+        if (__any_sync(0xffffffffu, need)) {
+          const float m_new = need ? mx : m_used;
           if (t > t0) {
-            // O holds PV(g-1) and earlier: wait for it, then scale the row in TMEM
-            const float f = ex2(m_used - m_new);
+            // O holds PV(g-1) and earlier: wait for it, then scale the rows in TMEM
+            const float f = need ? ex2(m_used - m_new) : 1.f;
             mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1

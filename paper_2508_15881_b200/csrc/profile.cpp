@@ -4,6 +4,8 @@
 // on the launching stream, so bench.py can attribute device time to each kernel live inside
 // its timed region (the events add no device work between the kernels).
 #include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -43,7 +45,7 @@ cudaEvent_t take_event() {
 }
 }  // namespace
 
-KernelScope::KernelScope(const char* name, cudaStream_t s) : stream(s) {
+KernelScope::KernelScope(const char* name, cudaStream_t s) : stream(s), name_(name) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (!g_profile_on.load(std::memory_order_relaxed)) return;
   std::lock_guard<std::mutex> lk(g_mu);
@@ -54,6 +56,13 @@ KernelScope::KernelScope(const char* name, cudaStream_t s) : stream(s) {
 }
 
 KernelScope::~KernelScope() {
+  static const bool debug_sync = getenv("TPLA_DEBUG_SYNC") != nullptr;
+  if (debug_sync) {
+    // diagnostic mode: run every launch to completion and name the kernel that faulted
+    cudaError_t e = cudaStreamSynchronize(stream);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) fprintf(stderr, "[tpla] kernel %s failed: %s\n", name_, cudaGetErrorString(e));
+  }
   if (slot < 0) return;
   std::lock_guard<std::mutex> lk(g_mu);
   if (slot < static_cast<int>(g_pending.size())) cudaEventRecord(g_pending[slot].stop, stream);

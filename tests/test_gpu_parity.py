@@ -198,6 +198,14 @@ def test_attention_parity_edge_lengths():
     attention_case(d, synth.PRESETS["dsv3"], 8, 2, [1500, 3], seed=4, peak=3.0)
 
 
+def test_attention_parity_divergent_rescale():
+    """Large logit spread over many sequences: the running max of different heads (TMEM lanes of
+    one warp) is raised at different tiles, so O rescales are per-row and warp-divergent."""
+    d = dev()
+    attention_case(d, synth.PRESETS["dsv3"], 2, 32, [2048] * 31 + [777], seed=5, peak=2.5)
+    attention_case(d, synth.PRESETS["dsv3"], 4, 16, [1000 + 37 * b for b in range(16)], seed=6, peak=3.0)
+
+
 # ----------------------------------------------------------------------------- end to end (K1..K5)
 def e2e_case(d, dims, k, g, kind, S_list, *, seed=0, modes=("exact", "sliced"), check_rank_parts=True):
     """All k ranks of a (k, g) plan run on this GPU, each accumulating into y (k-shard emulation);
