@@ -156,68 +156,79 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   const uint32_t tb = tmem_base;
   const Sched S = sch;
 
+
   if (warp == 0) {
-    // ============================================================ TMA producer
-    if (lane == 0) {
-      int g = 0;
-      for (int b = S.b_first; b <= S.b_last; ++b) {
-        const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
-        for (int t = t0; t < t1; ++t, ++g) {
-          const int st = g % C::NST;
-          mbar_wait(&kv_empty[st], ((g / C::NST) & 1) ^ 1);
+    // ============================================================ TMA producer (converged warp, one issuer)
+    int g = 0;
+    for (int b = S.b_first; b <= S.b_last; ++b) {
+      const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
+      const int* bt = a.block_table + (long)b * a.max_pages;
+      for (int t = t0; t < t1; ++t, ++g) {
+        const int st = g % C::NST;
+        mbar_wait(&kv_empty[st], ((g / C::NST) & 1) ^ 1);
+        if (elect_one()) {
           const int tok = (t - cum[b]) * kTile;
-          const int page = a.block_table[(long)b * a.max_pages + tok / a.page_size];
+          const int page = bt[tok / a.page_size];
           const int row = page * a.page_size + tok % a.page_size;
           uint8_t* dst = s_kv + st * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
 #pragma unroll
-          for (int j = 0; j < C::NBOX; ++j) tma_load_2d(dst + j * C::BOX_BYTES, &tmap, j * 64, row, &kv_full[st], kEvictFirst);
+          for (int j = 0; j < C::NBOX; ++j)
+            tma_load_2d(dst + j * C::BOX_BYTES, &tmap, j * 64, row, &kv_full[st], kEvictFirst);
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
-    // ============================================================ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t id_qk = idesc_bf16(128, kTile, false, false);
-      constexpr uint32_t id_pv = idesc_bf16(128, W_LAT, false, true);
-      const uint32_t qpe_addr = smem_addr(s_qpe);
-      int g = 0, seg = 0;
-      auto issue_pv = [&](int gp, bool first_pv) {
-        const int st = gp % C::NST;
-        mbar_wait(&p_full[gp & 1], (gp >> 1) & 1);
-        tc_fence_after();
-        const uint32_t kv = smem_addr(s_kv + st * C::STAGE_BYTES);
+    // ============================================================ MMA issuer (converged warp, one issuer)
+    constexpr uint32_t id_qk = idesc_bf16(128, kTile, false, false);
+    constexpr uint32_t id_pv = idesc_bf16(128, W_LAT, false, true);
+    constexpr uint32_t hi_k = desc_sw128_hi(1024);           // K-major: SBO = 1024 B (8-row groups)
+    const uint64_t qpe_desc = make_desc(smem_addr(s_qpe), 16, hi_k);
+    const uint32_t kv0 = smem_addr(s_kv);
+    int g = 0, seg = 0;
+    auto issue_pv = [&](int gp, bool first_pv) {
+      const int st = gp % C::NST;
+      mbar_wait(&p_full[gp & 1], (gp >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        // V = latent boxes of the tile, MN-major: 64-column atoms one box (8 KB) apart
+        const uint64_t v_desc = make_desc(kv0 + st * C::STAGE_BYTES, C::BOX_BYTES, hi_k);
         const uint32_t p_tmem = tb + C::S_COL0 + (gp & 1) * kTile;
 #pragma unroll
-        for (int kk = 0; kk < kTile / 16; ++kk)
-          mma_ts(tb + C::O_COL, p_tmem + kk * 8, desc_mnmajor_sw128(kv + kk * 2048, C::BOX_BYTES), id_pv,
+        for (int kk = 0; kk < kTile / 16; ++kk)      // 16 tokens (2 KB of rows) per step
+          mma_ts(tb + C::O_COL, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), id_pv,
                  (first_pv && kk == 0) ? 0u : 1u);
         mma_commit(&kv_empty[st]);
         mma_commit(&pv_done[gp & 1]);
-      };
-      for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
-        const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
-        mbar_wait(&q_ready, seg & 1);
+      }
+      __syncwarp();
+    };
+    for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
+      const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
+      mbar_wait(&q_ready, seg & 1);
+      tc_fence_after();
+      for (int t = t0; t < t1; ++t, ++g) {
+        const int st = g % C::NST;
+        mbar_wait(&kv_full[st], (g / C::NST) & 1);
         tc_fence_after();
-        for (int t = t0; t < t1; ++t, ++g) {
-          const int st = g % C::NST;
-          mbar_wait(&kv_full[st], (g / C::NST) & 1);
-          tc_fence_after();
-          const uint32_t kv = smem_addr(s_kv + st * C::STAGE_BYTES);
+        if (elect_one()) {
+          const uint64_t kv_desc = make_desc(kv0 + st * C::STAGE_BYTES, 16, hi_k);
           const uint32_t s_tmem = tb + C::S_COL0 + (g & 1) * kTile;
 #pragma unroll
-          for (int kk = 0; kk < W_LAT / 16; ++kk)     // Q'_j (TMEM) x ĉ tileᵀ
-            mma_ts(s_tmem, tb + C::Q_COL + kk * 8, desc_kmajor_sw128(kv + (kk >> 2) * C::BOX_BYTES + (kk & 3) * 32),
-                   id_qk, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < W_LAT / 16; ++kk)     // Q'_j (TMEM) x ĉ tileᵀ: box kk/4, +32 B per k-step
+            mma_ts(s_tmem, tb + C::Q_COL + kk * 8,
+                   kv_desc + uint64_t(((kk >> 2) * C::BOX_BYTES + (kk & 3) * 32) >> 4), id_qk, kk > 0 ? 1u : 0u);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)              // q^PE (smem) x k^PE tileᵀ
-            mma_ss(s_tmem, desc_kmajor_sw128(qpe_addr + kk * 32),
-                   desc_kmajor_sw128(kv + (C::NBOX - 1) * C::BOX_BYTES + kk * 32), id_qk, 1u);
+          for (int kk = 0; kk < 4; ++kk)              // q^PE (smem) x k^PE tileᵀ (last box)
+            mma_ss(s_tmem, qpe_desc + uint64_t(kk * 2),
+                   kv_desc + uint64_t(((C::NBOX - 1) * C::BOX_BYTES + kk * 32) >> 4), id_qk, 1u);
           mma_commit(&s_full[g & 1]);
-          if (t > t0) issue_pv(g - 1, t - 1 == t0);
         }
-        issue_pv(g - 1, t1 - 1 == t0);
+        __syncwarp();
+        if (t > t0) issue_pv(g - 1, t - 1 == t0);
       }
+      issue_pv(g - 1, t1 - 1 == t0);
     }
   } else if (warp >= 4) {
     // ============================================================ softmax / Q loader / epilogue
@@ -225,6 +236,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     const int r = q4 * 32 + lane;                       // head row = TMEM lane
     const uint32_t lane_base = tb + (uint32_t(q4 * 32) << 16);
     const bool row_ok = r < a.h_loc;
+    const float sc = a.scale_log2;
     int g = 0, seg = 0;
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
@@ -253,7 +265,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         tc_fence_before();
         mbar_arrive(&q_ready);
       }
-      float m_used = -INFINITY, l = 0.f;
+      float m_used = -INFINITY;                          // running max, log2 units
+      float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;      // running sum (4 chains)
       for (int t = t0; t < t1; ++t, ++g) {
         const int sb = g & 1;
         mbar_wait(&s_full[sb], (g >> 1) & 1);
@@ -262,15 +275,18 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         tmem_ld32(lane_base + C::S_COL0 + sb * kTile, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
         tmem_ld32(lane_base + C::S_COL0 + sb * kTile + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
         tmem_ld_wait();
-        const int tok0 = (t - cum[b]) * kTile;
-        const int nvalid = min(kTile, S_b - tok0);
-        float* x = reinterpret_cast<float*>(sv);
-        float mx = -INFINITY;
+        float* x = reinterpret_cast<float*>(sv);        // raw logits (sm_scale not applied yet)
+        const int nvalid = S_b - (t - cum[b]) * kTile;
+        if (nvalid < kTile) {                            // ragged last tile of the sequence
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          x[j] = j < nvalid ? x[j] * a.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, x[j]);
+          for (int j = 0; j < 64; ++j) x[j] = j < nvalid ? x[j] : -INFINITY;
         }
+        float m0 = x[0], m1 = x[1], m2 = x[2], m3 = x[3];
+#pragma unroll
+        for (int j = 4; j < 64; j += 4) {
+          m0 = fmaxf(m0, x[j]); m1 = fmaxf(m1, x[j + 1]); m2 = fmaxf(m2, x[j + 2]); m3 = fmaxf(m3, x[j + 3]);
+        }
+        const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sc;   // sc > 0: max commutes with scaling
         // Raise the running max only when it grew by more than 2^8 (p stays <= 256 in between).
         // The decision is per row, but the TMEM loads/stores of a rescale are warp-collective
         // (.sync.aligned), so the whole warp enters together; rows that keep their max scale by 1.
@@ -291,24 +307,26 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
               for (int j = 0; j < 32; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * f);
               tmem_st32(lane_base + C::O_COL + c0, ov);
             }
-            l *= f;
+            l0 *= f; l1 *= f; l2 *= f; l3 *= f;
           }
           m_used = m_new;
         }
+        const float neg_m = -m_used;
         uint32_t pw[32];
-        float ls = 0.f;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float p0 = ex2(x[2 * j] - m_used), p1 = ex2(x[2 * j + 1] - m_used);
-          ls += p0 + p1;
-          pw[j] = pack_bf16(p0, p1);
+        for (int j = 0; j < 32; j += 2) {
+          const float p0 = ex2(fmaf(x[2 * j], sc, neg_m)), p1 = ex2(fmaf(x[2 * j + 1], sc, neg_m));
+          const float p2 = ex2(fmaf(x[2 * j + 2], sc, neg_m)), p3 = ex2(fmaf(x[2 * j + 3], sc, neg_m));
+          l0 += p0; l1 += p1; l2 += p2; l3 += p3;
+          pw[j] = pack_bf16x2(p0, p1);
+          pw[j + 1] = pack_bf16x2(p2, p3);
         }
-        l += ls;
         tmem_st32(lane_base + C::S_COL0 + sb * kTile, pw);    // P over the first 32 columns of S(g)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
       }
+      const float l = (l0 + l1) + (l2 + l3);
       // ---- epilogue of the segment: unnormalised partial (O, m, l)
       mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
       tc_fence_after();
