@@ -31,7 +31,7 @@ def hadamard_U(d: int, seed: int | None) -> np.ndarray:
 
 def pca(features: np.ndarray, center: bool = False):
     """PCA basis of calibration latents F in R^{(B·L) x d} (§4.3.2):
-    eigendecomposition Sigma_F = U Λ U^T of the (uncentred by default, reading R8)
+    eigendecomposition Sigma_F = U Λ U^T of the (uncentred by default, reading R20)
     second-moment matrix.  Columns sorted by descending eigenvalue, ties by lower
     index; each column's largest-magnitude entry made positive.  Returns (U, λ)."""
     F = np.asarray(features, dtype=np.float64)
