@@ -40,7 +40,7 @@ namespace {
 using namespace sm100;
 
 constexpr int kTile = 64;         // tokens per tile
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;    // w0 TMA, w1 MMA, w2 TMEM alloc, w3 schedule, w4-w11 softmax
 constexpr int kMaxB = 512;        // sequences per launch supported by the smem schedule
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: p <= 2^8 between max updates
 
@@ -103,6 +103,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   __shared__ uint32_t tmem_base;
   __shared__ int cum[kMaxB + 1];
   __shared__ Sched sch;
+  __shared__ float red_max[2][2][128];   // [tile parity][half][row] partial row maxima
+  __shared__ float red_l[2][128];        // [half][row] partial row sums at a segment end
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int c = blockIdx.x, n_cta = gridDim.x;
@@ -111,8 +113,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap);
     for (int i = 0; i < C::NST; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 128); mbar_init(&pv_done[i], 1); }
-    mbar_init(&q_ready, 128);
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 256); mbar_init(&pv_done[i], 1); }
+    mbar_init(&q_ready, 256);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
@@ -232,31 +234,42 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     }
   } else if (warp >= 4) {
     // ============================================================ softmax / Q loader / epilogue
+    // Two warps per TMEM lane quadrant: warp 4+q handles S columns [0,32) (tokens 0-31 of the
+    // tile), warp 8+q columns [32,64), for the same 32 head rows; they exchange their partial
+    // row maxima through shared memory so both take the same rescale decisions.
     const int q4 = warp & 3;
+    const int half = (warp - 4) >> 2;                   // 0 or 1
     const int r = q4 * 32 + lane;                       // head row = TMEM lane
     const uint32_t lane_base = tb + (uint32_t(q4 * 32) << 16);
     const bool row_ok = r < a.h_loc;
     const float sc = a.scale_log2;
+    const uint32_t pair_bar = 1 + q4;                   // named barrier of the two warps of a quadrant
     int g = 0, seg = 0;
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
       const int S_b = min(a.seq_lens[b], a.cap);
-      // ---- Q'_j row -> TMEM (A operand, bf16 pairs per 32-bit column); q^PE row -> swizzled smem
+      // ---- Q'_j row -> TMEM (A operand, bf16 pairs per 32-bit column), half of it per warp;
+      //      q^PE row -> swizzled smem (chunks 4*half .. 4*half+3)
       {
         const uint4* src = reinterpret_cast<const uint4*>(a.q_lat + ((long)b * a.h_loc + r) * W_LAT);
+        constexpr int QC = W_LAT / 2;                   // packed columns of Q'_j
+        constexpr int QH = QC / 2 >= 32 ? QC / 2 : 32;  // columns per warp (W_LAT=64: one warp does all)
+        const int c_begin = QC / 2 >= 32 ? half * QH : 0;
+        if (QC / 2 >= 32 || half == 0) {
 #pragma unroll
-        for (int c0 = 0; c0 < W_LAT / 2; c0 += 32) {
-          uint32_t w[32];
+          for (int c0 = 0; c0 < QH; c0 += 32) {
+            uint32_t w[32];
 #pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            uint4 u = row_ok ? src[c0 / 4 + v] : make_uint4(0, 0, 0, 0);
-            w[4 * v] = u.x; w[4 * v + 1] = u.y; w[4 * v + 2] = u.z; w[4 * v + 3] = u.w;
+            for (int v = 0; v < 8; ++v) {
+              uint4 u = row_ok ? src[(c_begin + c0) / 4 + v] : make_uint4(0, 0, 0, 0);
+              w[4 * v] = u.x; w[4 * v + 1] = u.y; w[4 * v + 2] = u.z; w[4 * v + 3] = u.w;
+            }
+            tmem_st32(lane_base + C::Q_COL + c_begin + c0, w);
           }
-          tmem_st32(lane_base + C::Q_COL + c0, w);
         }
         const uint4* pe = reinterpret_cast<const uint4*>(a.q_pe + ((long)b * a.h_q + a.head_begin + r) * 64);
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
+        for (int ch = 4 * half; ch < 4 * half + 4; ++ch) {
           uint4 u = row_ok ? pe[ch] : make_uint4(0, 0, 0, 0);
           *reinterpret_cast<uint4*>(s_qpe + r * 128 + ((ch ^ (r & 7)) << 4)) = u;
         }
@@ -265,41 +278,43 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         tc_fence_before();
         mbar_arrive(&q_ready);
       }
-      float m_used = -INFINITY;                          // running max, log2 units
-      float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;      // running sum (4 chains)
+      float m_used = -INFINITY;                          // running max, log2 units (same in both halves)
+      float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;      // this half's running sum (4 chains)
       for (int t = t0; t < t1; ++t, ++g) {
         const int sb = g & 1;
         mbar_wait(&s_full[sb], (g >> 1) & 1);
         tc_fence_after();
-        uint32_t sv[64];
-        tmem_ld32(lane_base + C::S_COL0 + sb * kTile, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
-        tmem_ld32(lane_base + C::S_COL0 + sb * kTile + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
+        uint32_t sv[32];
+        tmem_ld32(lane_base + C::S_COL0 + sb * kTile + 32 * half, sv);
         tmem_ld_wait();
         float* x = reinterpret_cast<float*>(sv);        // raw logits (sm_scale not applied yet)
-        const int nvalid = S_b - (t - cum[b]) * kTile;
-        if (nvalid < kTile) {                            // ragged last tile of the sequence
+        const int nvalid = S_b - (t - cum[b]) * kTile - 32 * half;
+        if (nvalid < 32) {                               // ragged last tile of the sequence
 #pragma unroll
-          for (int j = 0; j < 64; ++j) x[j] = j < nvalid ? x[j] : -INFINITY;
+          for (int j = 0; j < 32; ++j) x[j] = j < nvalid ? x[j] : -INFINITY;
         }
         float m0 = x[0], m1 = x[1], m2 = x[2], m3 = x[3];
 #pragma unroll
-        for (int j = 4; j < 64; j += 4) {
+        for (int j = 4; j < 32; j += 4) {
           m0 = fmaxf(m0, x[j]); m1 = fmaxf(m1, x[j + 1]); m2 = fmaxf(m2, x[j + 2]); m3 = fmaxf(m3, x[j + 3]);
         }
-        const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sc;   // sc > 0: max commutes with scaling
+        float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+        red_max[sb][half][r] = mx;
+        named_bar_sync(pair_bar, 64);
+        mx = fmaxf(mx, red_max[sb][half ^ 1][r]) * sc;   // sc > 0: max commutes with scaling
         // Raise the running max only when it grew by more than 2^8 (p stays <= 256 in between).
-        // The decision is per row, but the TMEM loads/stores of a rescale are warp-collective
-        // (.sync.aligned), so the whole warp enters together; rows that keep their max scale by 1.
+        // The decision is per row (identical in both halves), but TMEM loads/stores are
+        // warp-collective (.sync.aligned), so a warp rescales if any of its rows needs it.
         const bool need = mx > m_used + kRescaleThreshold;
         if (__any_sync(0xffffffffu, need)) {
           const float m_new = need ? mx : m_used;
           if (t > t0) {
-            // O holds PV(g-1) and earlier: wait for it, then scale the rows in TMEM
+            // O holds PV(g-1) and earlier: wait for it, then scale this half's O columns
             const float f = need ? ex2(m_used - m_new) : 1.f;
             mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
-            for (int c0 = 0; c0 < W_LAT; c0 += 32) {
+            for (int c0 = half * (W_LAT / 2); c0 < (half + 1) * (W_LAT / 2); c0 += 32) {
               uint32_t ov[32];
               tmem_ld32(lane_base + C::O_COL + c0, ov);
               tmem_ld_wait();
@@ -312,29 +327,33 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           m_used = m_new;
         }
         const float neg_m = -m_used;
-        uint32_t pw[32];
+        uint32_t pw[16];
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
+        for (int j = 0; j < 16; j += 2) {
           const float p0 = ex2(fmaf(x[2 * j], sc, neg_m)), p1 = ex2(fmaf(x[2 * j + 1], sc, neg_m));
           const float p2 = ex2(fmaf(x[2 * j + 2], sc, neg_m)), p3 = ex2(fmaf(x[2 * j + 3], sc, neg_m));
           l0 += p0; l1 += p1; l2 += p2; l3 += p3;
           pw[j] = pack_bf16x2(p0, p1);
           pw[j + 1] = pack_bf16x2(p2, p3);
         }
-        tmem_st32(lane_base + C::S_COL0 + sb * kTile, pw);    // P over the first 32 columns of S(g)
+        // P (bf16 pairs) over columns [16*half, 16*half+16) of S(g): tokens 32*half .. +31
+        tmem_st16(lane_base + C::S_COL0 + sb * kTile + 16 * half, pw);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[sb]);
       }
-      const float l = (l0 + l1) + (l2 + l3);
       // ---- epilogue of the segment: unnormalised partial (O, m, l)
+      float l = (l0 + l1) + (l2 + l3);
+      red_l[half][r] = l;
       mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
       tc_fence_after();
+      named_bar_sync(pair_bar, 64);
+      l += red_l[half ^ 1][r];
       const int seg_id = S.seg_base + seg;
       {
         float* op = a.o_part + ((long)seg_id * a.h_loc + r) * W_LAT;
 #pragma unroll 1
-        for (int c0 = 0; c0 < W_LAT; c0 += 32) {
+        for (int c0 = half * (W_LAT / 2); c0 < (half + 1) * (W_LAT / 2); c0 += 32) {
           uint32_t ov[32];
           tmem_ld32(lane_base + C::O_COL + c0, ov);     // whole warp (.sync.aligned)
           tmem_ld_wait();
@@ -345,15 +364,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
                                                                     __uint_as_float(ov[j + 2]), __uint_as_float(ov[j + 3]));
           }
         }
-        if (row_ok) {
+        if (row_ok && half == 0) {
           a.ml_part[((long)seg_id * a.h_loc + r) * 2] = m_used;
           a.ml_part[((long)seg_id * a.h_loc + r) * 2 + 1] = l;
         }
       }
       // publish the sequence's segment range for K4: the CTA holding its first tile writes the
       // first segment id, the CTA holding its last tile the last one (ids are contiguous)
-      if (r == 0 && t0 == cum[b]) a.meta[2 * b] = seg_id;
-      if (r == 0 && t1 == cum[b + 1]) a.meta[2 * b + 1] = seg_id;
+      if (r == 0 && half == 0 && t0 == cum[b]) a.meta[2 * b] = seg_id;
+      if (r == 0 && half == 0 && t1 == cum[b + 1]) a.meta[2 * b + 1] = seg_id;
+      named_bar_sync(pair_bar, 64);                     // red_l free again
       tc_fence_before();
     }
   }
