@@ -28,6 +28,10 @@
 #include <cuda.h>
 #include <math.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -43,6 +47,7 @@ constexpr int kTile = 64;         // tokens per tile
 constexpr int kThreads = 384;    // w0 TMA, w1 MMA, w2 TMEM alloc, w3 schedule, w4-w11 softmax
 constexpr int kMaxB = 512;        // sequences per launch supported by the smem schedule
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: p <= 2^8 between max updates
+constexpr int kPrefetch = 0;      // tiles prefetched into L2 ahead of the smem ring (0: off, measured slower)
 
 struct TcArgs {
   const uint16_t* q_lat;       // [B, H_loc, W_lat]
@@ -55,7 +60,14 @@ struct TcArgs {
   int B, h_loc, h_q, head_begin, page_size, max_pages;
   int cap;                     // max_pages * page_size: lengths beyond the page table are clamped
   float scale_log2;
+  long long* trace;            // MODE 2 (diagnostic): clock64 stamps of CTA trace_cta, [4][kTrace]
+  int trace_cta;
 };
+constexpr int kTrace = 128;
+#define TRACE(slot, gg)                                                                  \
+  do {                                                                                   \
+    if (MODE == 2 && blockIdx.x == a.trace_cta && (gg) < kTrace) a.trace[(slot) * kTrace + (gg)] = clock64(); \
+  } while (0)
 
 template <int W_LAT>
 struct Cfg {
@@ -90,7 +102,9 @@ __device__ __forceinline__ int upper_bound_cum(const int* cum, int n, int x) {  
   return lo;
 }
 
-template <int W_LAT>
+// MODE 0: the kernel.  MODE 1 (diagnostic, TPLA_K3_MODE=stream): the TMA ring alone — every
+// tile is released as soon as it lands, no MMA/softmax — to measure the cache streaming rate.
+template <int W_LAT, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   using C = Cfg<W_LAT>;
@@ -155,30 +169,63 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (MODE == 2 && tid == 0) a.trace[4 * kTrace + 2 * c] = globaltimer();
   const uint32_t tb = tmem_base;
   const Sched S = sch;
 
 
   if (warp == 0) {
     // ============================================================ TMA producer (converged warp, one issuer)
-    int g = 0;
-    for (int b = S.b_first; b <= S.b_last; ++b) {
-      const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
-      const int* bt = a.block_table + (long)b * a.max_pages;
-      for (int t = t0; t < t1; ++t, ++g) {
-        const int st = g % C::NST;
-        mbar_wait(&kv_empty[st], ((g / C::NST) & 1) ^ 1);
-        if (elect_one()) {
-          const int tok = (t - cum[b]) * kTile;
-          const int page = bt[tok / a.page_size];
-          const int row = page * a.page_size + tok % a.page_size;
-          uint8_t* dst = s_kv + st * C::STAGE_BYTES;
-          mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
+    // Tile t of the flattened list -> cache row of its first token.  Tiles kPrefetch ahead are
+    // prefetched into L2 so that HBM requests stay in flight while the smem stages are held by
+    // QK -> softmax -> PV (stage hold time, not HBM, would otherwise set the streaming rate).
+    int b_ld = S.b_first, b_pf = S.b_first;
+    auto row_of = [&](int t, int& bb) {
+      while (cum[bb + 1] <= t) ++bb;
+      const int tok = (t - cum[bb]) * kTile;
+      const int page = a.block_table[(long)bb * a.max_pages + tok / a.page_size];
+      return page * a.page_size + tok % a.page_size;
+    };
+    for (int t = S.lo; kPrefetch > 0 && t < min(S.hi, S.lo + kPrefetch); ++t) {
+      const int row = row_of(t, b_pf);
+      if (elect_one()) {
 #pragma unroll
-          for (int j = 0; j < C::NBOX; ++j)
-            tma_load_2d(dst + j * C::BOX_BYTES, &tmap, j * 64, row, &kv_full[st], kEvictFirst);
+        for (int j = 0; j < C::NBOX; ++j) tma_prefetch_2d(&tmap, j * 64, row);
+      }
+      __syncwarp();
+    }
+    for (int t = S.lo, g = 0; t < S.hi; ++t, ++g) {
+      const int st = g % C::NST;
+      mbar_wait(&kv_empty[st], ((g / C::NST) & 1) ^ 1);
+      const int row_pf = (kPrefetch > 0 && t + kPrefetch < S.hi) ? row_of(t + kPrefetch, b_pf) : -1;
+      const int row = row_of(t, b_ld);
+      if (elect_one()) {
+        if (row_pf >= 0) {
+#pragma unroll
+          for (int j = 0; j < C::NBOX; ++j) tma_prefetch_2d(&tmap, j * 64, row_pf);
         }
+        uint8_t* dst = s_kv + st * C::STAGE_BYTES;
+        mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
+#pragma unroll
+        for (int j = 0; j < C::NBOX; ++j)
+          tma_load_2d(dst + j * C::BOX_BYTES, &tmap, j * 64, row, &kv_full[st], kEvictFirst);
+      }
+      __syncwarp();
+    }
+  } else if (MODE == 1 && warp == 1) {
+    int g = 0;
+    for (int b = S.b_first; b <= S.b_last; ++b)
+      for (int t = max(S.lo, cum[b]); t < min(S.hi, cum[b + 1]); ++t, ++g) {
+        mbar_wait(&kv_full[g % C::NST], (g / C::NST) & 1);
+        if (elect_one()) mbar_arrive(&kv_empty[g % C::NST]);
         __syncwarp();
+      }
+  } else if (MODE == 1) {
+    if (warp == 4 && lane == 0) {   // keep K4's segment map valid (values are meaningless)
+      int seg = 0;
+      for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
+        if (max(S.lo, cum[b]) == cum[b]) a.meta[2 * b] = S.seg_base + seg;
+        if (min(S.hi, cum[b + 1]) == cum[b + 1]) a.meta[2 * b + 1] = S.seg_base + seg;
       }
     }
   } else if (warp == 1) {
@@ -194,6 +241,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       mbar_wait(&p_full[gp & 1], (gp >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
+        TRACE(1, gp);
         // V = latent boxes of the tile, MN-major: 64-column atoms one box (8 KB) apart
         const uint64_t v_desc = make_desc(kv0 + st * C::STAGE_BYTES, C::BOX_BYTES, hi_k);
         const uint32_t p_tmem = tb + C::S_COL0 + (gp & 1) * kTile;
@@ -215,6 +263,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         mbar_wait(&kv_full[st], (g / C::NST) & 1);
         tc_fence_after();
         if (elect_one()) {
+          TRACE(0, g);
           const uint64_t kv_desc = make_desc(kv0 + st * C::STAGE_BYTES, 16, hi_k);
           const uint32_t s_tmem = tb + C::S_COL0 + (g & 1) * kTile;
 #pragma unroll
@@ -244,14 +293,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     const bool row_ok = r < a.h_loc;
     const float sc = a.scale_log2;
     const uint32_t pair_bar = 1 + q4;                   // named barrier of the two warps of a quadrant
-    int g = 0, seg = 0;
-    for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
-      const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
-      const int S_b = min(a.seq_lens[b], a.cap);
-      // ---- Q'_j row -> TMEM (A operand, bf16 pairs per 32-bit column), half of it per warp;
-      //      q^PE row -> swizzled smem (chunks 4*half .. 4*half+3)
-      {
-        const uint4* src = reinterpret_cast<const uint4*>(a.q_lat + ((long)b * a.h_loc + r) * W_LAT);
+    // Q'_j row -> TMEM (A operand, bf16 pairs per 32-bit column), half of it per warp;
+    // q^PE row -> swizzled smem (chunks 4*half .. 4*half+3); then signal the MMA warp
+    auto load_q = [&](int bb) {
+        const uint4* src = reinterpret_cast<const uint4*>(a.q_lat + ((long)bb * a.h_loc + r) * W_LAT);
         constexpr int QC = W_LAT / 2;                   // packed columns of Q'_j
         constexpr int QH = QC / 2 >= 32 ? QC / 2 : 32;  // columns per warp (W_LAT=64: one warp does all)
         const int c_begin = QC / 2 >= 32 ? half * QH : 0;
@@ -267,7 +312,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
             tmem_st32(lane_base + C::Q_COL + c_begin + c0, w);
           }
         }
-        const uint4* pe = reinterpret_cast<const uint4*>(a.q_pe + ((long)b * a.h_q + a.head_begin + r) * 64);
+        const uint4* pe = reinterpret_cast<const uint4*>(a.q_pe + ((long)bb * a.h_q + a.head_begin + r) * 64);
 #pragma unroll
         for (int ch = 4 * half; ch < 4 * half + 4; ++ch) {
           uint4 u = row_ok ? pe[ch] : make_uint4(0, 0, 0, 0);
@@ -277,12 +322,18 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&q_ready);
-      }
+    };
+    int g = 0, seg = 0;
+    if (S.b_first <= S.b_last) load_q(S.b_first);
+    for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
+      const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
+      const int S_b = min(a.seq_lens[b], a.cap);
       float m_used = -INFINITY;                          // running max, log2 units (same in both halves)
       float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;      // this half's running sum (4 chains)
       for (int t = t0; t < t1; ++t, ++g) {
         const int sb = g & 1;
         mbar_wait(&s_full[sb], (g >> 1) & 1);
+        if (warp == 4 && lane == 0) TRACE(2, g);
         tc_fence_after();
         uint32_t sv[32];
         tmem_ld32(lane_base + C::S_COL0 + sb * kTile + 32 * half, sv);
@@ -340,8 +391,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         tmem_st16(lane_base + C::S_COL0 + sb * kTile + 16 * half, pw);
         tmem_st_wait();
         tc_fence_before();
+        if (warp == 4 && lane == 0) TRACE(3, g);
         mbar_arrive(&p_full[sb]);
       }
+      // The segment's QKs are all complete (its last S was just consumed): stage the next
+      // segment's Q now, so its first QKs run on the tensor pipe during this epilogue.  Its
+      // first PV still waits for this epilogue: it needs p_full, which these warps signal later.
+      if (b < S.b_last) load_q(b + 1);
       // ---- epilogue of the segment: unnormalised partial (O, m, l)
       float l = (l0 + l1) + (l2 + l3);
       red_l[half][r] = l;
@@ -381,6 +437,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (MODE == 2 && tid == 0) a.trace[4 * kTrace + 2 * c + 1] = globaltimer();
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tb);
 }
 
@@ -446,18 +503,55 @@ int num_sms() {
   return n;
 }
 
-template <int W_LAT>
-cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaStream_t s) {
+template <int W_LAT, int MODE>
+cudaError_t launch_tc_mode(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaStream_t s) {
   using C = Cfg<W_LAT>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<W_LAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(attn_tc_kernel<W_LAT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  KernelScope ks("K3_attn_tc", s);
-  attn_tc_kernel<W_LAT><<<n_cta, kThreads, C::SMEM, s>>>(map, a);
+  KernelScope ks(MODE == 0 ? "K3_attn_tc" : "K3_stream_only", s);
+  attn_tc_kernel<W_LAT, MODE><<<n_cta, kThreads, C::SMEM, s>>>(map, a);
   return cudaGetLastError();
+}
+
+template <int W_LAT>
+cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaStream_t s) {
+  static const char* mode = getenv("TPLA_K3_MODE");
+  if (mode && strcmp(mode, "stream") == 0) return launch_tc_mode<W_LAT, 1>(map, a, n_cta, s);
+  if (mode && strcmp(mode, "trace") == 0) {
+    static long long* buf = nullptr;
+    const int nb = 4 * kTrace + 2 * n_cta;
+    if (!buf) cudaMalloc(&buf, (4 * kTrace + 2 * 1024) * sizeof(long long));
+    TcArgs b = a;
+    b.trace = buf;
+    const char* tc = getenv("TPLA_K3_TRACE_CTA");
+    b.trace_cta = tc ? atoi(tc) : 0;
+    cudaError_t e = launch_tc_mode<W_LAT, 2>(map, b, n_cta, s);
+    static long long h[4 * kTrace + 2 * 1024];
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h, buf, nb * sizeof(long long), cudaMemcpyDeviceToHost);
+    long long t0 = h[4 * kTrace], t1 = 0, s_max = 0;
+    for (int c = 0; c < n_cta; ++c) {
+      t0 = std::min(t0, h[4 * kTrace + 2 * c]);
+      t1 = std::max(t1, h[4 * kTrace + 2 * c + 1]);
+    }
+    for (int c = 0; c < n_cta; ++c) {
+      long long st = h[4 * kTrace + 2 * c] - t0, en = h[4 * kTrace + 2 * c + 1] - t0;
+      s_max = std::max(s_max, st);
+      if (c % 8 == 0) fprintf(stderr, "[k3 cta] %3d start %6lld ns end %6lld ns\n", c, st, en);
+    }
+    fprintf(stderr, "[k3 cta] span %lld ns, latest start %lld ns\n", t1 - t0, s_max);
+    fprintf(stderr, "[k3 trace] g qk_issue pv_issue(g) s_ready(g) p_done(g) (cycles rel. to qk_issue[0])\n");
+    for (int g = 0; g < kTrace; ++g)
+      fprintf(stderr, "[k3 trace] %2d %8lld %8lld %8lld %8lld\n", g, h[g] - h[0], h[kTrace + g] - h[0],
+              h[2 * kTrace + g] - h[0], h[3 * kTrace + g] - h[0]);
+    return e;
+  }
+  return launch_tc_mode<W_LAT, 0>(map, a, n_cta, s);
 }
 
 }  // namespace
@@ -491,6 +585,7 @@ cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const 
   a.B = B; a.h_loc = g.h_loc; a.h_q = g.h_q; a.head_begin = g.head_begin; a.page_size = cache.page_size;
   a.max_pages = cache.max_pages_per_seq; a.scale_log2 = g.sm_scale * 1.4426950408889634f;
   a.cap = cache.max_pages_per_seq * cache.page_size;
+  a.trace = nullptr;
   switch (g.w_lat) {
     case 64: return launch_tc<64>(map, a, n_cta, s);
     case 128: return launch_tc<128>(map, a, n_cta, s);
