@@ -47,7 +47,8 @@ constexpr int kTile = 64;         // tokens per tile
 constexpr int kThreads = 384;    // w0 TMA, w1 MMA, w2 TMEM alloc, w3 schedule, w4-w11 softmax
 constexpr int kMaxB = 512;        // sequences per launch supported by the smem schedule
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: p <= 2^8 between max updates
-constexpr int kPrefetch = 0;      // tiles prefetched into L2 ahead of the smem ring (0: off, measured slower)
+// L2 prefetch distance (tiles beyond the smem ring) comes from TcArgs::prefetch (TPLA_K3_PREFETCH,
+// default 0: an 8-tile distance measured slower)
 
 struct TcArgs {
   const uint16_t* q_lat;       // [B, H_loc, W_lat]
@@ -62,6 +63,7 @@ struct TcArgs {
   float scale_log2;
   long long* trace;            // MODE 2 (diagnostic): clock64 stamps of CTA trace_cta, [4][kTrace]
   int trace_cta;
+  int prefetch;                // tiles prefetched into L2 ahead of the smem ring (0 = off)
 };
 constexpr int kTrace = 128;
 #define TRACE(slot, gg)                                                                  \
@@ -92,6 +94,24 @@ struct Sched {
   int b_first, b_last;
   int seg_base;
 };
+
+// Work split with a fixed cost per sequence start: sequence b occupies kSeqCost work units of
+// "header" (its Q load, pipeline refill and the previous segment's epilogue) followed by one
+// unit per tile, so a CTA whose range crosses a sequence boundary gets fewer tiles.  tile_of maps
+// a work position to the first tile at or after it.
+constexpr int kSeqCost = 8;
+__device__ __forceinline__ int tile_of(const int* cum, int B, long w) {
+  int lo = 0, hi = B + 1;                       // first b with cum[b] + kSeqCost*b > w
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if ((long)cum[mid] + (long)kSeqCost * mid <= w) lo = mid + 1; else hi = mid;
+  }
+  const int b = lo - 1;
+  const long off = w - ((long)cum[b] + (long)kSeqCost * b) - kSeqCost;
+  long t = cum[b] + (off > 0 ? off : 0);
+  if (b < B && t > cum[b + 1]) t = cum[b + 1];
+  return int(t);
+}
 
 __device__ __forceinline__ int upper_bound_cum(const int* cum, int n, int x) {  // first i with cum[i] > x
   int lo = 0, hi = n;
@@ -149,20 +169,27 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     }
     if (lane == 0) cum[a.B] = carry;
     __syncwarp();
-    const long T = carry;
+    const long Wt = long(carry) + long(kSeqCost) * a.B;     // total work units
+    auto range = [&](int cc, int& lo, int& hi) {
+      lo = tile_of(cum, a.B, cc * Wt / n_cta);
+      hi = tile_of(cum, a.B, (cc + 1) * Wt / n_cta);
+    };
     // segments of CTAs c' < c (each CTA range touches b_last - b_first + 1 sequences)
     int before = 0;
     for (int cc = lane; cc < c; cc += 32) {
-      int lo = int(cc * T / n_cta), hi = int((cc + 1) * T / n_cta);
+      int lo, hi;
+      range(cc, lo, hi);
       if (lo < hi) before += upper_bound_cum(cum, a.B + 1, hi - 1) - upper_bound_cum(cum, a.B + 1, lo) + 1;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
     if (lane == 0) {
-      sch.lo = int(c * T / n_cta);
-      sch.hi = int((c + 1) * T / n_cta);
-      sch.b_first = sch.lo < sch.hi ? upper_bound_cum(cum, a.B + 1, sch.lo) - 1 : 0;
-      sch.b_last = sch.lo < sch.hi ? upper_bound_cum(cum, a.B + 1, sch.hi - 1) - 1 : -1;
+      int lo, hi;
+      range(c, lo, hi);
+      sch.lo = lo;
+      sch.hi = hi;
+      sch.b_first = lo < hi ? upper_bound_cum(cum, a.B + 1, lo) - 1 : 0;
+      sch.b_last = lo < hi ? upper_bound_cum(cum, a.B + 1, hi - 1) - 1 : -1;
       sch.seg_base = before;
     }
   }
@@ -186,6 +213,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       const int page = a.block_table[(long)bb * a.max_pages + tok / a.page_size];
       return page * a.page_size + tok % a.page_size;
     };
+    const int kPrefetch = a.prefetch;
     for (int t = S.lo; kPrefetch > 0 && t < min(S.hi, S.lo + kPrefetch); ++t) {
       const int row = row_of(t, b_pf);
       if (elect_one()) {
@@ -586,6 +614,9 @@ cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const 
   a.max_pages = cache.max_pages_per_seq; a.scale_log2 = g.sm_scale * 1.4426950408889634f;
   a.cap = cache.max_pages_per_seq * cache.page_size;
   a.trace = nullptr;
+  a.trace_cta = 0;
+  static const char* pf = getenv("TPLA_K3_PREFETCH");
+  a.prefetch = pf ? atoi(pf) : 0;
   switch (g.w_lat) {
     case 64: return launch_tc<64>(map, a, n_cta, s);
     case 128: return launch_tc<128>(map, a, n_cta, s);
