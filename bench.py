@@ -61,6 +61,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
     p.add_argument("--batch", type=int, default=None, help="override the workload batch (sweep)")
     p.add_argument("--seq-len", type=int, default=None, help="override the workload context length (sweep)")
+    p.add_argument("--no-graph", action="store_true", help="issue the timed steps eagerly instead of a CUDA graph")
     p.add_argument("--profile-region", action="store_true",
                    help="cudaProfilerStart/Stop around the timed region (for ncu --profile-from-start off)")
     return p.parse_args()
@@ -360,26 +361,76 @@ def main():
     abi.tpla_sync(stream.cuda_stream)
 
     # ---- timed region (device-timed with CUDA events on the launching stream)
+    # The K steps are captured once as a CUDA graph (every library call is async on the stream,
+    # NCCL included) and replayed: no host launch overhead inside the region.  The library's
+    # per-kernel profile events are captured too, as event nodes between the kernels.
+    # Two identical captures: `graph` (no profiling) times the value; `graph_prof` (with the
+    # library's event nodes around every kernel) is replayed right after for the per-kernel times.
     abi.tpla_profile_reset()
-    abi.tpla_profile_enable(True)
+    n0 = abi.tpla_launch_count()
+    graph = graph_prof = breakdown = None
+    k3_q = [torch.randn((B, rk.plan.h_loc, rk.plan.w_lat), generator=gen, device=dev).to(torch.bfloat16) for rk in ranks]
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+            for i in range(args.steps):
+                step(i)
+        launches = abi.tpla_launch_count() - n0           # kernels in the K timed steps
+        abi.tpla_profile_enable(1)                       # events around every kernel (breakdown)
+        graph_all = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_all, capture_error_mode="relaxed"):
+            for i in range(args.steps):
+                step(i)
+        abi.tpla_profile_enable(False)
+        # the event nodes add gaps between kernels, so these durations are upper bounds
+        graph_all.replay()
+        torch.cuda.synchronize()
+        breakdown = abi.profile_table()
+        abi.tpla_profile_reset()
+        # K3 alone: the attention launches of the K steps (same kernel, same cache, Q' of the
+        # same shape), back to back with no event nodes; outer events give its launch duration
+        graph_prof = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_prof, capture_error_mode="relaxed"):
+            for i in range(args.steps):
+                for j, rk in enumerate(ranks):
+                    rk.decode_attention(k3_q[j], qp[i % NP], seq_lens, None)     # K3 alone
+        stream = torch.cuda.current_stream()
+        graph.replay()                                   # untimed warm replay
+        torch.cuda.synchronize()
+    else:
+        abi.tpla_profile_enable(True)
     barrier()
     torch.cuda.synchronize()
-    n0 = abi.tpla_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if args.profile_region:
         torch.cuda.cudart().cudaProfilerStart()
     with ClockSampler(local) as clocks:
         ev0.record(stream)
-        for i in range(args.steps):
-            step(i)
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(args.steps):
+                step(i)
         ev1.record(stream)
         torch.cuda.synchronize()
     if args.profile_region:
         torch.cuda.cudart().cudaProfilerStop()
     barrier()
-    launches = abi.tpla_launch_count() - n0
+    ms_prof = None
+    if graph_prof is not None:
+        torch.cuda.synchronize()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        graph_prof.replay()
+        p1.record(stream)
+        torch.cuda.synchronize()
+        ms_prof = p0.elapsed_time(p1) / (args.steps * len(ranks))   # ms per isolated K3 launch
+        prof = breakdown                                 # in-step durations (roofline)
+    else:
+        launches = abi.tpla_launch_count() - n0
+        prof = abi.profile_table()
+        breakdown = prof
     abi.tpla_profile_enable(False)
-    prof = abi.profile_table()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = ms / args.steps
     value = B * args.steps / (ms / 1e3)
@@ -404,16 +455,17 @@ def main():
             traffic = tr[k3_name]["dram_bytes_per_launch"]
     except Exception:
         pass
-    step_gpu_ms = sum(v[0] for v in prof.values()) / args.steps
+    step_gpu_ms = ms_step                                  # clean (unprofiled) step time
     roofline = {"bound": bound, "achieved": gbs if bound == "hbm" else tfs, "peak": hbm if bound == "hbm" else tf_burst,
                 "unit": "GB/s" if bound == "hbm" else "TFLOP/s", "frac": (gbs / hbm) if bound == "hbm" else (tfs / tf_burst),
                 "traffic": traffic, "kernel": k3_name, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_k3, "algorithmic_flops_per_launch": flops_k3,
                 "avg_launch_us": k3_avg_s * 1e6, "launches": k3_n,
+                "isolated_avg_launch_us": ms_prof * 1e3 if ms_prof else None,
                 "tensor_tflops": tfs, "tensor_frac_of_burst": tfs / tf_burst,
                 "share_of_step": (k3_ms / args.steps) / step_gpu_ms if step_gpu_ms > 0 else None}
     kernels = {n: {"us_per_step": v[0] / args.steps * 1e3, "launches_per_step": v[1] / args.steps}
-               for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+               for n, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])}
 
     # ---- end to end through the public API with host buffers (pinned), copies inside the region
     e2e = None
@@ -429,7 +481,13 @@ def main():
         d2h = h_out.numel() * h_out.element_size()
         n_e2e = max(10, min(args.steps, 100))
         for i in range(3):
-            step(i)
+            step(i, d_ck, d_kp, d_q, d_qp)
+        g1 = None
+        if not args.no_graph:                         # one decode step (K1..K5, C1) as a graph
+            g1 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g1, capture_error_mode="relaxed"):
+                step(0, d_ck, d_kp, d_q, d_qp)
+            stream = torch.cuda.current_stream()
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -440,7 +498,10 @@ def main():
             d_kp.copy_(h_kp[j], non_blocking=True)
             d_q.copy_(h_q[j], non_blocking=True)
             d_qp.copy_(h_qp[j], non_blocking=True)
-            step(i, d_ck, d_kp, d_q, d_qp)
+            if g1 is not None:
+                g1.replay()
+            else:
+                step(i, d_ck, d_kp, d_q, d_qp)
             h_out.copy_(out, non_blocking=True)
             stream.synchronize()          # the host consumes each step's output before the next
         e1.record(stream)
@@ -463,6 +524,12 @@ def main():
                 "data": "synthetic", "impl": "tpla", "config": config_of(wl, N, k, g),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "gpu_launches_per_step": launches / args.steps, "clocks": clocks.summary(), "kernels": kernels,
+                "cuda_graph": graph is not None,
+                "kernel_timing": ("library CUDA events (on the launching stream) captured as graph event nodes "
+                                  "around every kernel of the K timed steps, replayed right after the timed "
+                                  "replay (the nodes add small gaps: durations are upper bounds); "
+                                  "roofline.isolated_avg_launch_us: a graph of the K3 launches alone"
+                                  if graph is not None else "library CUDA events inside the timed region"),
                 "hbm_gbs_per_gpu_k3": gbs, "kv_bytes_per_gpu_per_step": bytes_k3 * len(ranks)}
         print(json.dumps(line), flush=True)
     if N > 1:

@@ -199,7 +199,8 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
 /* K3 + K4 only (attention of one shard, Eq. tpla_softmax_one_device without W^VO):
  *   q_lat: device bf16 [B, H_loc, W_lat] (= Q'_j, mu_j included); q_pe: device bf16 [B, h_q, d_r]
  *   (all heads); O: device fp32 [B, H_loc, W_lat] = Σ_t p_t ĉ_{j,t};  lse: device fp32 [B, H_loc]
- *   or NULL: log Σ_t exp(s_t) (natural log, s_t including sm_scale). */
+ *   or NULL: log Σ_t exp(s_t) (natural log, s_t including sm_scale).  O = lse = NULL runs K3 alone
+ *   (its partials stay in the workspace): used to time the attention kernel by itself. */
 tpla_status tpla_decode_attention(const tpla_config* cfg, const tpla_cache* cache, const void* q_lat,
                                   const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t max_seq_len,
                                   void* ws, size_t ws_bytes, float* O, float* lse, void* stream);
@@ -218,8 +219,9 @@ tpla_status tpla_sync(void* stream);
 
 /* ---- measurement: per-kernel device time --------------------------------------------- */
 
-/* When on != 0, every kernel launch of this library is bracketed by two CUDA events recorded
- * on its launching stream (no device work is added).  Host-side bookkeeping only. */
+/* on = 1: every kernel launch of this library is bracketed by two CUDA events recorded on its
+ * launching stream (no device work is added; under stream capture they become event nodes);
+ * on = 2: only the decode-attention kernel (K3) is bracketed; on = 0: off. */
 tpla_status tpla_profile_enable(int32_t on);
 /* Wait for the recorded events and accumulate their elapsed times per kernel name. */
 tpla_status tpla_profile_collect(void);

@@ -47,10 +47,11 @@ cudaEvent_t take_event() {
 
 KernelScope::KernelScope(const char* name, cudaStream_t s) : stream(s), name_(name) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (!g_profile_on.load(std::memory_order_relaxed)) return;
+  const int mode = g_profile_on.load(std::memory_order_relaxed);
+  if (!mode || (mode == 2 && strncmp(name, "K3", 2) != 0)) return;   // mode 2: the attention kernel only
   std::lock_guard<std::mutex> lk(g_mu);
   Pending p{name, take_event(), take_event()};
-  cudaEventRecord(p.start, s);
+  cudaEventRecordWithFlags(p.start, s, cudaEventRecordExternal);  // external: an event node under graph capture
   g_pending.push_back(p);
   slot = static_cast<int>(g_pending.size()) - 1;
 }
@@ -65,7 +66,7 @@ KernelScope::~KernelScope() {
   }
   if (slot < 0) return;
   std::lock_guard<std::mutex> lk(g_mu);
-  if (slot < static_cast<int>(g_pending.size())) cudaEventRecord(g_pending[slot].stop, stream);
+  if (slot < static_cast<int>(g_pending.size())) cudaEventRecordWithFlags(g_pending[slot].stop, stream, cudaEventRecordExternal);
 }
 
 }  // namespace tpla
@@ -75,7 +76,7 @@ using namespace tpla;
 extern "C" {
 
 tpla_status tpla_profile_enable(int32_t on) {
-  g_profile_on.store(on ? 1 : 0);
+  g_profile_on.store(on == 2 ? 2 : (on ? 1 : 0));
   return TPLA_OK;
 }
 

@@ -235,12 +235,12 @@ static cudaError_t run_attention(const Geom& g, const tpla_cache& cache, const u
   if (use_tc) {
     auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
     e = launch_decode_attn_tc(g, cache, q_lat, q_pe, seq_lens, B, L.n_cta, o_part, ml_part, meta, s);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess || (!o_bf16 && !o_f32 && !lse)) return e;   // no output requested: K3 alone
     return launch_combine_seg(g, B, o_part, ml_part, meta, o_bf16, o_f32, lse, s);
   }
   SplitPlan sp = choose_split(B, max_seq_len);
   e = launch_decode_attn(g, cache, q_lat, q_pe, seq_lens, B, sp, o_part, ml_part, s);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || (!o_bf16 && !o_f32 && !lse)) return e;   // no output requested: K3 alone
   return launch_combine(g, B, sp, o_part, ml_part, o_bf16, o_f32, lse, s);
 }
 
@@ -527,7 +527,8 @@ tpla_status tpla_decode_attention(const tpla_config* cfg, const tpla_cache* cach
   tpla_status st = make_geom(cfg, &g);
   if (st) return st;
   if ((st = check_decode_common(g, cache, q_pe, seq_lens, B, max_seq_len))) return st;
-  if (!q_lat || !O || !ws) return fail(TPLA_ERR_INVALID_ARG, "NULL q_lat/O/ws");
+  if (!q_lat || !ws) return fail(TPLA_ERR_INVALID_ARG, "NULL q_lat/ws");
+  if (!O && lse) return fail(TPLA_ERR_INVALID_ARG, "lse requires O");
   if (!aligned16(q_lat) || !aligned16(ws)) return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
   WsLayout L = ws_layout(g, B, max_seq_len);
   if (ws_bytes < L.total) return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, L.total);
