@@ -97,7 +97,8 @@ typedef struct tpla_device_plan {
 typedef struct tpla_weights {
   void* W_UK;         /* bf16 [H_loc, W_lat, d_h]: mu_j · (U^T W_γ W^UK)[lat rows, head h cols]   */
   void* W_UV;         /* bf16 [H_loc, d_h, W_lat]: (U^T W_γ W^UV)[lat rows, head h cols]^T         */
-  void* W_O;          /* bf16 [D, H_loc·d_h]: (W^O[head rows of block i, :])^T                      */
+  void* W_O;          /* bf16 (W^O[head rows of block i, :])^T, K = H_loc·d_h: if 64 | K blocked
+                         [ceil(D/128)][K/64][128][64] (rows >= D zero), else [D, K]               */
   void* xform;        /* fp32: HADAMARD [d_c] signs ±1; PCA [d_c, W_lat] = U[:, lat range]; else NULL */
   int32_t xform_kind; /* TPLA_XFORM_*                                                              */
   float alpha_j;      /* Condition 1 constant of this shard                     */

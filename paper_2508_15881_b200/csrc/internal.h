@@ -48,6 +48,7 @@ struct WsLayout {
   size_t v;         // bf16 [B, H_loc*d_h]
   size_t y_part;    // fp32 [kslices, B, D]
   size_t meta;      // int32 [B, 2] (persistent K3: first segment id, count)
+  size_t wo_part;   // persistent W^O GEMM partials + segment map
   size_t total;
   int kslices;
   int n_cta;        // persistent K3 grid
@@ -86,6 +87,15 @@ cudaError_t launch_combine_seg(const Geom& g, int B, const float* o_part, const 
 // y_part[ks, b, n] = sum_{k in slice ks} Wt[n, k] * v[b, k]; Wt [N, K] bf16, v [B, K] bf16.
 cudaError_t launch_skinny_gemm(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, int kslices,
                                float* y_part, cudaStream_t s);
+
+// Blackwell-native W^O up-projection (tcgen05 + TMA, persistent split-K) with its segment reduce:
+// y[b, n] (=|+=) Σ_k v[b, k] Wt[n, k].  part_ws: wo_tc_part_bytes(N, K, B) bytes of workspace.
+bool wo_tc_supported(int N, int K, int B);
+// W^O is stored blocked [ceil(D/128)][K/64][128][64] when 64 | K (the tcgen05 path), else [D, K]
+inline bool wo_blocked(int K) { return K % 64 == 0; }
+size_t wo_tc_part_bytes(int N, int K, int B);
+cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, void* part_ws, float* y,
+                         bool accumulate, cudaStream_t s);
 
 // y[b, n] (=|+=) sum_ks y_part[ks, b, n]
 cudaError_t launch_reduce_slices(const float* y_part, int kslices, int B, int N, float* y, bool accumulate,

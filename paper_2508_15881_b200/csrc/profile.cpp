@@ -33,6 +33,15 @@ std::vector<Pending> g_pending;
 std::vector<cudaEvent_t> g_free;
 std::vector<Acc> g_acc;
 
+// Under stream capture the record must be an external event node (so the graph records a
+// timestamp); outside capture the flag is not valid and a plain record is used.
+void record(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &st);
+  if (st == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else cudaEventRecord(e, s);
+}
+
 cudaEvent_t take_event() {
   if (!g_free.empty()) {
     cudaEvent_t e = g_free.back();
@@ -51,7 +60,7 @@ KernelScope::KernelScope(const char* name, cudaStream_t s) : stream(s), name_(na
   if (!mode || (mode == 2 && strncmp(name, "K3", 2) != 0)) return;   // mode 2: the attention kernel only
   std::lock_guard<std::mutex> lk(g_mu);
   Pending p{name, take_event(), take_event()};
-  cudaEventRecordWithFlags(p.start, s, cudaEventRecordExternal);  // external: an event node under graph capture
+  record(p.start, s);
   g_pending.push_back(p);
   slot = static_cast<int>(g_pending.size()) - 1;
 }
@@ -66,7 +75,7 @@ KernelScope::~KernelScope() {
   }
   if (slot < 0) return;
   std::lock_guard<std::mutex> lk(g_mu);
-  if (slot < static_cast<int>(g_pending.size())) cudaEventRecordWithFlags(g_pending[slot].stop, stream, cudaEventRecordExternal);
+  if (slot < static_cast<int>(g_pending.size())) record(g_pending[slot].stop, stream);
 }
 
 }  // namespace tpla

@@ -219,6 +219,7 @@ WsLayout ws_layout(const Geom& g, int B, int max_seq_len) {
   L.v = off;       off += align256(size_t(B) * K * 2);
   L.y_part = off;  off += align256(size_t(L.kslices) * B * g.D * 4);
   L.meta = off;    off += align256(size_t(B) * 2 * 4);
+  L.wo_part = off; off += align256(wo_tc_supported(g.D, K, B) ? wo_tc_part_bytes(g.D, K, B) : 0);
   L.total = off;
   return L;
 }
@@ -300,7 +301,10 @@ tpla_status tpla_weights_bytes(const tpla_config* cfg, int32_t xform_kind, size_
   if (st) return st;
   if (W_UK) *W_UK = size_t(g.h_loc) * g.w_lat * g.d_h * 2;
   if (W_UV) *W_UV = size_t(g.h_loc) * g.d_h * g.w_lat * 2;
-  if (W_O) *W_O = size_t(g.D) * g.h_loc * g.d_h * 2;
+  if (W_O) {
+    const int K = g.h_loc * g.d_h;
+    *W_O = (wo_blocked(K) ? size_t((g.D + 127) / 128) * 128 : size_t(g.D)) * K * 2;
+  }
   if (xform) {
     if (xform_kind == TPLA_XFORM_HADAMARD) *xform = size_t(g.d_c) * 4;
     else if (xform_kind == TPLA_XFORM_PCA) *xform = size_t(g.d_c) * g.w_lat * 4;
@@ -376,12 +380,22 @@ tpla_status tpla_convert_weights(const tpla_config* cfg, int32_t xform_kind, uin
       uv[(size_t(h) * d_h + e) * WL + l] = double_to_bf16(tb[l]);
     }
   });
-  // W^O rows of head block i, transposed to [D, H*d_h] (K-major for the up-projection GEMM)
+  // W^O rows of head block i, transposed to K-major for the up-projection GEMM: blocked
+  // [ceil(D/128)][K/64][128][64] (each 128-row x 64-k tile one contiguous 16 KB block for the
+  // TMA weight stream, rows >= D zero) when 64 | K, else plain [D, K]
   const int K = H * d_h;
-  std::vector<uint16_t> wo(size_t(D) * K);
+  const bool blocked = wo_blocked(K);
+  const int n_tiles = (D + 127) / 128, k_steps = K / 64;
+  std::vector<uint16_t> wo(blocked ? size_t(n_tiles) * 128 * K : size_t(D) * K, 0);
   parallel_for(K, [&](int kk) {
     const uint16_t* src = W_O + (size_t(g.head_begin) * d_h + kk) * D;
-    for (int n = 0; n < D; ++n) wo[size_t(n) * K + kk] = src[n];
+    if (blocked) {
+      const int ks = kk / 64, kc = kk % 64;
+      for (int n = 0; n < D; ++n)
+        wo[((size_t(n / 128) * k_steps + ks) * 128 + n % 128) * 64 + kc] = src[n];
+    } else {
+      for (int n = 0; n < D; ++n) wo[size_t(n) * K + kk] = src[n];
+    }
   });
   std::vector<float> xf;
   if (xform_kind == TPLA_XFORM_HADAMARD) {
@@ -502,11 +516,19 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
   e = launch_head_gemv("K5_W_UV", static_cast<const uint16_t*>(w->W_UV), o_lat, long(g.h_loc) * g.w_lat, g.h_loc, g.d_h,
                        g.w_lat, B, v, s);
   if (e != cudaSuccess) return cuda_fail(e, "K5a W_UV");
-  // K5b: Õ_j = v W^O_rows
-  e = launch_skinny_gemm(static_cast<const uint16_t*>(w->W_O), v, g.D, g.h_loc * g.d_h, B, L.kslices, y_part, s);
-  if (e != cudaSuccess) return cuda_fail(e, "K5b W_O");
-  e = launch_reduce_slices(y_part, L.kslices, B, g.D, y, (flags & TPLA_DECODE_ACCUMULATE) != 0, s);
-  if (e != cudaSuccess) return cuda_fail(e, "K5b reduce");
+  // K5b: Õ_j = v W^O_rows — tcgen05 weight stream where the shapes allow
+  const bool accumulate = (flags & TPLA_DECODE_ACCUMULATE) != 0;
+  const int Kw = g.h_loc * g.d_h;
+  const char* force = getenv("TPLA_WO");
+  if (wo_tc_supported(g.D, Kw, B) && !(force && strcmp(force, "mma") == 0)) {
+    e = launch_wo_tc(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, B, base + L.wo_part, y, accumulate, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K5b W_O (tcgen05)");
+  } else {
+    e = launch_skinny_gemm(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, B, L.kslices, y_part, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K5b W_O");
+    e = launch_reduce_slices(y_part, L.kslices, B, g.D, y, accumulate, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K5b reduce");
+  }
   // C1: O = AllReduce(Σ_r Õ_r)
   if (comm) {
     ncclResult_t r = g_nccl.AllReduce(y, y, size_t(B) * g.D, ncclFloat32, ncclSum, comm->comm, s);
