@@ -33,6 +33,8 @@ struct AppendArgs {
 
 template <int E>
 __global__ void __launch_bounds__(128) append_kernel(AppendArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (row >= a.n) return;
@@ -156,8 +158,7 @@ cudaError_t launch_E(const AppendArgs& a, cudaStream_t s) {
   int blocks = (a.n + 3) / 4;
   size_t smem = (a.xform_kind == TPLA_XFORM_PCA) ? size_t(4) * a.d_c * sizeof(float) : 0;
   KernelScope ks("K1_append_kv", s);
-  append_kernel<E><<<blocks, 128, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(append_kernel<E>, blocks, 128, smem, s, a);
 }
 
 }  // namespace

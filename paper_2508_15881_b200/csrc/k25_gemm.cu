@@ -31,6 +31,8 @@ struct GemmArgs {
 __device__ __forceinline__ int swz(int row, int chunk) { return row * BK + ((chunk ^ (row & 7)) << 3); }
 
 __global__ void __launch_bounds__(THREADS) nt_gemm_kernel(GemmArgs g) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(128) uint16_t smem[];
   uint16_t* sA = smem;
   uint16_t* sB = smem + STAGES * A_TILE;
@@ -139,12 +141,13 @@ cudaError_t launch_nt(const GemmArgs& a, int Z, const char* name, cudaStream_t s
   }
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, Z);
   KernelScope ks(name, s);
-  nt_gemm_kernel<<<grid, THREADS, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(nt_gemm_kernel, grid, THREADS, smem, s, a);
 }
 
 __global__ void reduce_slices_kernel(const float* __restrict__ y_part, int kslices, long n, float* __restrict__ y,
                                      int accumulate) {
+  pdl_trigger();
+  pdl_wait();
   long i = (blockIdx.x * (long)blockDim.x + threadIdx.x) * 4;
   if (i >= n) return;
   float4 acc = accumulate ? *reinterpret_cast<const float4*>(y + i) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -156,6 +159,8 @@ __global__ void reduce_slices_kernel(const float* __restrict__ y_part, int kslic
 }
 
 __global__ void cast_kernel(const float* __restrict__ y, long n, uint16_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   long i = (blockIdx.x * (long)blockDim.x + threadIdx.x) * 4;
   if (i >= n) return;
   float4 v = *reinterpret_cast<const float4*>(y + i);
@@ -193,15 +198,13 @@ cudaError_t launch_reduce_slices(const float* y_part, int kslices, int B, int N,
   long n = (long)B * N;  // N % 8 == 0 (validated) so n % 4 == 0
   int blocks = (int)((n / 4 + 255) / 256);
   KernelScope ks("K5_reduce", s);
-  reduce_slices_kernel<<<blocks, 256, 0, s>>>(y_part, kslices, n, y, accumulate ? 1 : 0);
-  return cudaGetLastError();
+  return launch_k(reduce_slices_kernel, blocks, 256, 0, s, y_part, kslices, n, y, accumulate ? 1 : 0);
 }
 
 cudaError_t launch_cast_bf16(const float* y, long n, uint16_t* out, cudaStream_t s) {
   int blocks = (int)((n / 4 + 255) / 256);
   KernelScope ks("C1_cast_bf16", s);
-  cast_kernel<<<blocks, 256, 0, s>>>(y, n, out);
-  return cudaGetLastError();
+  return launch_k(cast_kernel, blocks, 256, 0, s, y, n, out);
 }
 
 }  // namespace tpla

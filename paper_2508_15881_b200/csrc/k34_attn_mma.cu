@@ -36,6 +36,8 @@ struct AttnArgs {
 
 template <int W_LAT, int D_R>
 __global__ void __launch_bounds__(256, 1) attn_mma_kernel(AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int W = W_LAT + D_R;
   constexpr int WP = W + 8;                 // padded row: odd number of 16-byte chunks -> no ldmatrix conflicts
   constexpr int KSTEPS = W / 16;
@@ -204,14 +206,15 @@ cudaError_t launch_attn_t(const AttnArgs& a, int B, cudaStream_t s) {
   }
   dim3 grid(a.n_split, B);
   KernelScope ks("K3_attn_mma", s);
-  attn_mma_kernel<W_LAT, D_R><<<grid, nwarps * 32, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(attn_mma_kernel<W_LAT, D_R>, grid, nwarps * 32, smem, s, a);
 }
 
 // K4: O = Σ_s 2^{m_s - M} O_s / Σ_s 2^{m_s - M} l_s
 __global__ void combine_kernel(const float* __restrict__ o_part, const float* __restrict__ ml_part, int n_split,
                                int h_loc, int w_lat, uint16_t* __restrict__ o_bf16, float* __restrict__ o_f32,
                                float* __restrict__ lse) {
+  pdl_trigger();
+  pdl_wait();
   const int h = blockIdx.x, b = blockIdx.y;
   const long base = (long)b * n_split;
   float M = -INFINITY;
@@ -272,8 +275,8 @@ cudaError_t launch_combine(const Geom& g, int B, const SplitPlan& sp, const floa
   dim3 grid(g.h_loc, B);
   int threads = std::min(64, std::max(32, g.w_lat / 4));
   KernelScope ks("K4_combine", s);
-  combine_kernel<<<grid, threads, 0, s>>>(o_part, ml_part, sp.n_split, g.h_loc, g.w_lat, o_bf16, o_f32, lse);
-  return cudaGetLastError();
+  return launch_k(combine_kernel, grid, threads, 0, s, o_part, ml_part, sp.n_split, g.h_loc, g.w_lat, o_bf16,
+                  o_f32, lse);
 }
 
 }  // namespace tpla

@@ -127,6 +127,7 @@ __device__ __forceinline__ int upper_bound_cum(const int* cum, int n, int x) {  
 template <int W_LAT, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
+  pdl_trigger();
   using C = Cfg<W_LAT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -152,6 +153,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
+  pdl_wait();   // everything below reads the predecessors' outputs (seq_lens, Q', cache rows)
   if (warp == 3) {
     // tiles per sequence -> exclusive prefix sum (warp scan, 32 sequences per step)
     int carry = 0;
@@ -474,6 +476,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
 __global__ void combine_seg_kernel(const float* __restrict__ o_part, const float* __restrict__ ml_part,
                                    const int32_t* __restrict__ meta, int h_loc, int w_lat,
                                    uint16_t* __restrict__ o_bf16, float* __restrict__ o_f32, float* __restrict__ lse) {
+  pdl_trigger();
+  pdl_wait();
   const int h = blockIdx.x, b = blockIdx.y;
   const int s0 = meta[2 * b], ns = meta[2 * b + 1] - s0 + 1;
   float M = -INFINITY;
@@ -542,8 +546,7 @@ cudaError_t launch_tc_mode(const CUtensorMap& map, const TcArgs& a, int n_cta, c
     attr = true;
   }
   KernelScope ks(MODE == 0 ? "K3_attn_tc" : "K3_stream_only", s);
-  attn_tc_kernel<W_LAT, MODE><<<n_cta, kThreads, C::SMEM, s>>>(map, a);
-  return cudaGetLastError();
+  return launch_k(attn_tc_kernel<W_LAT, MODE>, n_cta, kThreads, C::SMEM, s, map, a);
 }
 
 template <int W_LAT>
@@ -630,8 +633,8 @@ cudaError_t launch_combine_seg(const Geom& g, int B, const float* o_part, const 
   dim3 grid(g.h_loc, B);
   int threads = std::min(64, std::max(32, g.w_lat / 4));
   KernelScope ks("K4_combine", s);
-  combine_seg_kernel<<<grid, threads, 0, s>>>(o_part, ml_part, meta, g.h_loc, g.w_lat, o_bf16, o_f32, lse);
-  return cudaGetLastError();
+  return launch_k(combine_seg_kernel, grid, threads, 0, s, o_part, ml_part, meta, g.h_loc, g.w_lat, o_bf16, o_f32,
+                  lse);
 }
 
 }  // namespace tpla

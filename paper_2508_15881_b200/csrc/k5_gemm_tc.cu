@@ -46,6 +46,7 @@ struct GCfg {
 template <int NP>
 __global__ void __launch_bounds__(256, 1)
 skinny_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, GArgs a) {
+  pdl_trigger();
   using C = GCfg<NP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -76,6 +77,7 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
+  pdl_wait();   // v (and y) come from the predecessors
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -167,6 +169,8 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
 // y[b, n] = (accumulate ? y[b, n] : 0) + Σ_{seg of tile n/128} part[seg, b, n % 128]   (fixed order)
 __global__ void reduce_seg_kernel(const float* __restrict__ part, const int32_t* __restrict__ meta, int N, int B,
                                   float* __restrict__ y, int accumulate) {
+  pdl_trigger();
+  pdl_wait();
   const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (i >= (long)B * N) return;
   const int b = int(i / N), n = int(i % N), rt = n / kTM;
@@ -224,8 +228,7 @@ cudaError_t launch_np(const CUtensorMap& mA, const CUtensorMap& mB, const GArgs&
     attr = true;
   }
   KernelScope ks("K5_W_O_tc", s);
-  skinny_tc_kernel<NP><<<n_cta, 256, C::SMEM, s>>>(mA, mB, a);
-  return cudaGetLastError();
+  return launch_k(skinny_tc_kernel<NP>, n_cta, 256, C::SMEM, s, mA, mB, a);
 }
 
 }  // namespace
@@ -268,8 +271,7 @@ cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, in
   if (e != cudaSuccess) return e;
   const long n = long(B) * N;
   KernelScope ks("K5_reduce", s);
-  reduce_seg_kernel<<<int((n + 255) / 256), 256, 0, s>>>(a.part, a.meta, N, B, y, accumulate ? 1 : 0);
-  return cudaGetLastError();
+  return launch_k(reduce_seg_kernel, int((n + 255) / 256), 256, 0, s, a.part, a.meta, N, B, y, accumulate ? 1 : 0);
 }
 
 }  // namespace tpla

@@ -54,6 +54,14 @@ cudaEvent_t take_event() {
 }
 }  // namespace
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TPLA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 KernelScope::KernelScope(const char* name, cudaStream_t s) : stream(s), name_(name) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   const int mode = g_profile_on.load(std::memory_order_relaxed);
