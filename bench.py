@@ -446,7 +446,11 @@ def main():
     k3_avg_s = k3_ms / max(k3_n, 1) / 1e3
     gbs = bytes_k3 / k3_avg_s / 1e9
     tfs = flops_k3 / k3_avg_s / 1e12
-    bound = "hbm" if bytes_k3 / (hbm * 1e9) >= flops_k3 / (tf_burst * 1e12) else "tensor"
+    # K3 is timed inside a long step: the tensor peak is the SUSTAINED bf16 figure (power-capped
+    # clocks, B200_PROFILING.md); the binding roofline is the slower of bytes/HBM and FLOPs/tensor
+    tf_peak = tf_sust if tf_sust > 0 else tf_burst
+    t_hbm_s, t_tc_s = bytes_k3 / (hbm * 1e9), flops_k3 / (tf_peak * 1e12)
+    bound = "hbm" if t_hbm_s >= t_tc_s else "tensor"
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -456,13 +460,16 @@ def main():
     except Exception:
         pass
     step_gpu_ms = ms_step                                  # clean (unprofiled) step time
-    roofline = {"bound": bound, "achieved": gbs if bound == "hbm" else tfs, "peak": hbm if bound == "hbm" else tf_burst,
-                "unit": "GB/s" if bound == "hbm" else "TFLOP/s", "frac": (gbs / hbm) if bound == "hbm" else (tfs / tf_burst),
-                "traffic": traffic, "kernel": k3_name, "peak_source": peak_src,
+    roofline = {"bound": bound, "achieved": gbs if bound == "hbm" else tfs, "peak": hbm if bound == "hbm" else tf_peak,
+                "unit": "GB/s" if bound == "hbm" else "TFLOP/s", "frac": (gbs / hbm) if bound == "hbm" else (tfs / tf_peak),
+                "traffic": traffic, "kernel": k3_name,
+                "peak_source": f"{peak_src} (MEASURED_PEAKS.json: hbm_gbs, bf16_tflops_sustained)",
+                "roofline_time_us": {"hbm": t_hbm_s * 1e6, "tensor_sustained": t_tc_s * 1e6},
+                "hbm_gbs": gbs, "hbm_frac": gbs / hbm,
                 "algorithmic_bytes_per_launch": bytes_k3, "algorithmic_flops_per_launch": flops_k3,
                 "avg_launch_us": k3_avg_s * 1e6, "launches": k3_n,
                 "isolated_avg_launch_us": ms_prof * 1e3 if ms_prof else None,
-                "tensor_tflops": tfs, "tensor_frac_of_burst": tfs / tf_burst,
+                "tensor_tflops": tfs, "tensor_frac_of_sustained": tfs / tf_peak, "tensor_frac_of_burst": tfs / tf_burst,
                 "share_of_step": (k3_ms / args.steps) / step_gpu_ms if step_gpu_ms > 0 else None}
     kernels = {n: {"us_per_step": v[0] / args.steps * 1e3, "launches_per_step": v[1] / args.steps}
                for n, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])}

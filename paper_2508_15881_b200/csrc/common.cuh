@@ -11,6 +11,9 @@ namespace tpla {
 // its predecessor's completion + memory flush (pdl_wait) only before touching its outputs.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// A kernel that does not read its predecessor's output (K1 append, K2 absorb) waits at its END
+// instead: it overlaps the predecessor, and its completion still implies the predecessor's, so
+// completion stays transitive along the stream for the kernels that wait at entry.
 
 bool pdl_enabled();   // TPLA_PDL=0 disables (host)
 

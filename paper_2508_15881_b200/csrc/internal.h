@@ -65,8 +65,9 @@ cudaError_t launch_append_kv(const Geom& g, int xform_kind, const float* xform, 
 
 // out[b, h, r] = sum_c W[h, r, c] * x[b, h, c]     (K2 with R=W_lat,C=d_h; K5a with R=d_h,C=W_lat)
 // x has row stride x_head_stride elements between heads and x_batch_stride between batches.
+// inputs_from_host: x/W are not written by the preceding kernel (PDL: overlap it, wait at the end)
 cudaError_t launch_head_gemv(const char* name, const uint16_t* W, const uint16_t* x, long x_batch_stride, int H,
-                             int R, int C, int B, uint16_t* out_bf16, cudaStream_t s);
+                             int R, int C, int B, uint16_t* out_bf16, bool inputs_from_host, cudaStream_t s);
 
 cudaError_t launch_decode_attn(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat,
                                const uint16_t* q_pe, const int32_t* seq_lens, int B, const SplitPlan& sp,
@@ -83,6 +84,11 @@ cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const 
                                   int32_t* meta, cudaStream_t s);
 cudaError_t launch_combine_seg(const Geom& g, int B, const float* o_part, const float* ml_part, const int32_t* meta,
                                uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s);
+
+// K4 + K5a fused (persistent-K3 partials): v[b, h, :] = combine(partials)[b, h, :] · W^UV'_j[h]ᵀ
+bool combine_wuv_supported(const Geom& g);
+cudaError_t launch_combine_wuv(const Geom& g, int B, const float* o_part, const float* ml_part, const int32_t* meta,
+                               const uint16_t* W_UV, uint16_t* v, cudaStream_t s);
 
 // y_part[ks, b, n] = sum_{k in slice ks} Wt[n, k] * v[b, k]; Wt [N, K] bf16, v [B, K] bf16.
 cudaError_t launch_skinny_gemm(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, int kslices,

@@ -32,9 +32,17 @@ struct AppendArgs {
 };
 
 template <int E>
+__device__ __forceinline__ void append_row(const AppendArgs& a);
+
+template <int E>
 __global__ void __launch_bounds__(128) append_kernel(AppendArgs a) {
   pdl_trigger();
-  pdl_wait();
+  append_row<E>(a);
+  pdl_wait();   // inputs come from the host / earlier copies: wait only to keep completion transitive
+}
+
+template <int E>
+__device__ __forceinline__ void append_row(const AppendArgs& a) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (row >= a.n) return;

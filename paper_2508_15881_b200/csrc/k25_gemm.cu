@@ -25,14 +25,22 @@ struct GemmArgs {
   int M, N, K;
   // output: bf16 (out_bf16 != null) at out + z*o_zs + m*o_ms + n, else fp32 at out_f32 + ...
   uint16_t* out_bf16; float* out_f32; long o_zs, o_ms;
+  int inputs_from_host;   // 1: A/Bw are not written by the preceding kernel (PDL wait at the end)
 };
+
+__device__ __forceinline__ void nt_gemm_body(const GemmArgs& g);
 
 // swizzled element offset of (row, chunk-of-8) in a [rows][64] bf16 tile
 __device__ __forceinline__ int swz(int row, int chunk) { return row * BK + ((chunk ^ (row & 7)) << 3); }
 
 __global__ void __launch_bounds__(THREADS) nt_gemm_kernel(GemmArgs g) {
   pdl_trigger();
-  pdl_wait();
+  if (!g.inputs_from_host) pdl_wait();
+  nt_gemm_body(g);
+  if (g.inputs_from_host) pdl_wait();   // K2: q comes from the caller, wait only for transitivity
+}
+
+__device__ __forceinline__ void nt_gemm_body(const GemmArgs& g) {
   extern __shared__ __align__(128) uint16_t smem[];
   uint16_t* sA = smem;
   uint16_t* sB = smem + STAGES * A_TILE;
@@ -173,8 +181,9 @@ __global__ void cast_kernel(const float* __restrict__ y, long n, uint16_t* __res
 }  // namespace
 
 cudaError_t launch_head_gemv(const char* name, const uint16_t* W, const uint16_t* x, long x_batch_stride, int H,
-                             int R, int C, int B, uint16_t* out_bf16, cudaStream_t s) {
+                             int R, int C, int B, uint16_t* out_bf16, bool inputs_from_host, cudaStream_t s) {
   GemmArgs a{};
+  a.inputs_from_host = inputs_from_host ? 1 : 0;
   a.A = x; a.a_zs = C; a.a_ms = x_batch_stride;
   a.Bw = W; a.b_zs = (long)R * C; a.b_ns = C;
   a.M = B; a.N = R; a.K = C;

@@ -225,15 +225,18 @@ WsLayout ws_layout(const Geom& g, int B, int max_seq_len) {
 }
 
 // K3 + K4: the tcgen05 kernel where its shapes allow (TPLA_ATTN=mma forces the legacy path)
+static bool use_tc_attention(const Geom& g, int B) {
+  const char* force = getenv("TPLA_ATTN");
+  return tc_attention_supported(g, B) && !(force && strcmp(force, "mma") == 0);
+}
+
 static cudaError_t run_attention(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
                                  const int32_t* seq_lens, int B, int max_seq_len, const WsLayout& L, char* base,
                                  uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s) {
   auto* o_part = reinterpret_cast<float*>(base + L.o_part);
   auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
-  const char* force = getenv("TPLA_ATTN");
-  const bool use_tc = tc_attention_supported(g, B) && !(force && strcmp(force, "mma") == 0);
   cudaError_t e;
-  if (use_tc) {
+  if (use_tc_attention(g, B)) {
     auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
     e = launch_decode_attn_tc(g, cache, q_lat, q_pe, seq_lens, B, L.n_cta, o_part, ml_part, meta, s);
     if (e != cudaSuccess || (!o_bf16 && !o_f32 && !lse)) return e;   // no output requested: K3 alone
@@ -506,16 +509,29 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
   cudaError_t e;
   // K2: Q'_j[b,h,:] = W^UK'_j[h] q[b,h,:]   (mu_j folded)
   e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK), qn + size_t(g.head_begin) * g.d_h,
-                       long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h, B, q_lat, s);
+                       long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h, B, q_lat, true, s);
   if (e != cudaSuccess) return cuda_fail(e, "K2 absorb_q");
-  // K3 + K4: per-shard split-K flash decoding (Eq. tpla_softmax_one_device) -> O_j
-  e = run_attention(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, max_seq_len, L, base, o_lat,
-                    nullptr, nullptr, s);
-  if (e != cudaSuccess) return cuda_fail(e, "K3/K4 decode attention");
-  // K5a: v[b,h,:] = W^UV'_j[h]^T-applied O_j  (W^VO factored)
-  e = launch_head_gemv("K5_W_UV", static_cast<const uint16_t*>(w->W_UV), o_lat, long(g.h_loc) * g.w_lat, g.h_loc, g.d_h,
-                       g.w_lat, B, v, s);
-  if (e != cudaSuccess) return cuda_fail(e, "K5a W_UV");
+  if (use_tc_attention(g, B) && combine_wuv_supported(g)) {
+    // K3: per-shard split-K flash decoding (Eq. tpla_softmax_one_device) -> partials;
+    // K4 + K5a fused: merge the partials of each (b, h) into O_j and apply W^UV'_j
+    auto* o_part = reinterpret_cast<float*>(base + L.o_part);
+    auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
+    auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
+    e = launch_decode_attn_tc(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, L.n_cta, o_part,
+                              ml_part, meta, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K3 decode attention");
+    e = launch_combine_wuv(g, B, o_part, ml_part, meta, static_cast<const uint16_t*>(w->W_UV), v, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K4+K5a combine/W_UV");
+  } else {
+    // K3 + K4: per-shard split-K flash decoding (Eq. tpla_softmax_one_device) -> O_j
+    e = run_attention(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, max_seq_len, L, base, o_lat,
+                      nullptr, nullptr, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K3/K4 decode attention");
+    // K5a: v[b,h,:] = W^UV'_j[h]^T-applied O_j  (W^VO factored)
+    e = launch_head_gemv("K5_W_UV", static_cast<const uint16_t*>(w->W_UV), o_lat, long(g.h_loc) * g.w_lat, g.h_loc,
+                         g.d_h, g.w_lat, B, v, false, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K5a W_UV");
+  }
   // K5b: Õ_j = v W^O_rows — tcgen05 weight stream where the shapes allow
   const bool accumulate = (flags & TPLA_DECODE_ACCUMULATE) != 0;
   const int Kw = g.h_loc * g.d_h;
