@@ -46,6 +46,7 @@ using namespace sm100;
 constexpr int kTile = 64;         // tokens per tile
 constexpr int kThreads = 384;    // w0 TMA, w1 MMA, w2 TMEM alloc, w3 schedule, w4-w11 softmax
 constexpr int kMaxB = 512;        // sequences per launch supported by the smem schedule
+constexpr int kMaxCta = 256;      // persistent grid bound (<= #SMs in practice)
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: p <= 2^8 between max updates
 // L2 prefetch distance (tiles beyond the smem ring) comes from TcArgs::prefetch (TPLA_K3_PREFETCH,
 // default 0: an 8-tile distance measured slower)
@@ -137,7 +138,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   __shared__ uint64_t s_full[2], p_full[2], pv_done[2], q_ready;
   __shared__ uint32_t tmem_base;
   __shared__ int cum[kMaxB + 1];
-  __shared__ Sched sch;
+  __shared__ int lo_arr[kMaxCta + 1];    // first tile of every CTA's range (+ the end)
+  __shared__ int s_before;
   __shared__ float red_max[2][2][128];   // [tile parity][half][row] partial row maxima
   __shared__ float red_l[2][128];        // [half][row] partial row sums at a segment end
 
@@ -153,6 +155,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
+  if (tid == 0) s_before = 0;
   pdl_wait();   // everything below reads the predecessors' outputs (seq_lens, Q', cache rows)
   if (warp == 3) {
     // tiles per sequence -> exclusive prefix sum (warp scan, 32 sequences per step)
@@ -170,37 +173,38 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       carry += __shfl_sync(0xffffffffu, x, 31);
     }
     if (lane == 0) cum[a.B] = carry;
-    __syncwarp();
-    const long Wt = long(carry) + long(kSeqCost) * a.B;     // total work units
-    auto range = [&](int cc, int& lo, int& hi) {
-      lo = tile_of(cum, a.B, cc * Wt / n_cta);
-      hi = tile_of(cum, a.B, (cc + 1) * Wt / n_cta);
-    };
-    // segments of CTAs c' < c (each CTA range touches b_last - b_first + 1 sequences)
+  }
+  __syncthreads();
+  // Every CTA needs the ranges of all CTAs before it (its first segment id = the number of
+  // segments they produce).  All threads share that work — one range start per thread — so no
+  // CTA pays a serial loop over its predecessors (that loop staggered the CTA starts by up to
+  // 6.7 us at 148 CTAs).
+  {
+    const long Wt = long(cum[a.B]) + long(kSeqCost) * a.B;     // total work units
+    for (int cc = tid; cc <= n_cta; cc += kThreads) lo_arr[cc] = tile_of(cum, a.B, cc * Wt / n_cta);
+  }
+  __syncthreads();
+  {
     int before = 0;
-    for (int cc = lane; cc < c; cc += 32) {
-      int lo, hi;
-      range(cc, lo, hi);
+    for (int cc = tid; cc < c; cc += kThreads) {
+      const int lo = lo_arr[cc], hi = lo_arr[cc + 1];
       if (lo < hi) before += upper_bound_cum(cum, a.B + 1, hi - 1) - upper_bound_cum(cum, a.B + 1, lo) + 1;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
-    if (lane == 0) {
-      int lo, hi;
-      range(c, lo, hi);
-      sch.lo = lo;
-      sch.hi = hi;
-      sch.b_first = lo < hi ? upper_bound_cum(cum, a.B + 1, lo) - 1 : 0;
-      sch.b_last = lo < hi ? upper_bound_cum(cum, a.B + 1, hi - 1) - 1 : -1;
-      sch.seg_base = before;
-    }
+    if (lane == 0 && before) atomicAdd(&s_before, before);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (MODE == 2 && tid == 0) a.trace[4 * kTrace + 2 * c] = globaltimer();
   const uint32_t tb = tmem_base;
-  const Sched S = sch;
+  Sched S;
+  S.lo = lo_arr[c];
+  S.hi = lo_arr[c + 1];
+  S.b_first = S.lo < S.hi ? upper_bound_cum(cum, a.B + 1, S.lo) - 1 : 0;
+  S.b_last = S.lo < S.hi ? upper_bound_cum(cum, a.B + 1, S.hi - 1) - 1 : -1;
+  S.seg_base = s_before;
 
 
   if (warp == 0) {
@@ -593,7 +597,7 @@ bool tc_attention_supported(const Geom& g, int B) {
 
 int tc_num_ctas(int B, int max_seq_len) {
   long tiles = (long)B * ((max_seq_len + kTile - 1) / kTile);
-  return int(std::max(1L, std::min<long>(num_sms(), tiles)));
+  return int(std::max(1L, std::min<long>(std::min(num_sms(), kMaxCta), tiles)));
 }
 
 cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,

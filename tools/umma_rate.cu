@@ -1,0 +1,97 @@
+// Throughput probe of tcgen05.mma kind::f16 shapes (one CTA per SM, one elected issuer):
+// cycles per MMA instruction and the implied dense bf16 rate for the shapes K3 uses and the
+// alternatives (A from smem = SS, A from TMEM = TS; N = 64 / 128 / 256).  Operand contents are
+// irrelevant (zeros); the point is the issue/execute rate of back-to-back MMAs.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -I paper_2508_15881_b200/csrc tools/umma_rate.cu -o /tmp/umma_rate
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "sm100.cuh"
+
+using namespace tpla::sm100;
+
+constexpr int kIters = 4096;
+
+template <int N, bool TS, bool B_MN>
+__global__ void rate_kernel(long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 65536 / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  if (warp == 0) tmem_alloc<512>(&tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tmem_base;
+  if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(128, N, false, B_MN);
+    constexpr uint32_t hi = desc_sw128_hi(1024);
+    const uint64_t da = make_desc(smem_addr(smem), 16, hi);
+    const uint64_t db = make_desc(smem_addr(smem + 16384), B_MN ? 8192 : 16, hi);
+    long long t0 = 0;
+    if (elect_one()) {
+      t0 = clock64();
+      for (int it = 0; it < kIters; ++it) {
+        const uint32_t d = tb;   // one accumulator chain, as in a GEMM k-loop
+        if (TS) mma_ts(d, tb + 256 + (it & 3) * 8, db + uint64_t((it & 3) * 2), idesc, 1u);
+        else mma_ss(d, da + uint64_t((it & 3) * 2), db + uint64_t((it & 3) * 2), idesc, 1u);
+      }
+      mma_commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    if (elect_one()) cyc[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<512>(tb);
+}
+
+template <int N, bool TS, bool B_MN>
+void run(const char* name, int n_cta) {
+  long long* d;
+  cudaMalloc(&d, n_cta * sizeof(long long));
+  auto k = rate_kernel<N, TS, B_MN>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024 + 1024);
+  k<<<n_cta, 128, 66 * 1024 + 1024>>>(d);   // warm-up
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  k<<<n_cta, 128, 66 * 1024 + 1024>>>(d);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(err)); exit(1); }
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  long long h[148];
+  cudaMemcpy(h, d, n_cta * sizeof(long long), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < n_cta; ++i) avg += h[i];
+  avg /= n_cta;
+  const double flops = 2.0 * 128 * N * 16 * kIters * n_cta;
+  printf("%-22s N=%3d  %6.1f cyc/mma (floor %3d)  %7.1f TFLOP/s (event %.1f us)\n", name, N, avg / kIters,
+         128 * N / 256, flops / (ms * 1e-3) / 1e12, ms * 1e3);
+  cudaFree(d);
+}
+
+int main() {
+  int n = 148;
+  run<64, false, false>("SS K-major", n);
+  run<64, true, false>("TS K-major", n);
+  run<128, false, false>("SS K-major", n);
+  run<128, true, false>("TS K-major", n);
+  run<256, false, false>("SS K-major", n);
+  run<256, true, false>("TS K-major", n);
+  run<256, true, true>("TS MN-major (PV)", n);
+  run<128, true, true>("TS MN-major", n);
+  run<64, true, false>("TS K-major 1 CTA", 1);
+  run<256, true, true>("TS MN-major 1 CTA", 1);
+  printf("RATE OK\n");
+  return 0;
+}
