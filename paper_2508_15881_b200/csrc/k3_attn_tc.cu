@@ -48,8 +48,6 @@ constexpr int kThreads = 384;    // w0 TMA, w1 MMA, w2 TMEM alloc, w3 schedule, 
 constexpr int kMaxB = 512;        // sequences per launch supported by the smem schedule
 constexpr int kMaxCta = 256;      // persistent grid bound (<= #SMs in practice)
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: p <= 2^8 between max updates
-// L2 prefetch distance (tiles beyond the smem ring) comes from TcArgs::prefetch (TPLA_K3_PREFETCH,
-// default 0: an 8-tile distance measured slower)
 
 struct TcArgs {
   const uint16_t* q_lat;       // [B, H_loc, W_lat]
@@ -64,12 +62,13 @@ struct TcArgs {
   float scale_log2;
   long long* trace;            // MODE 2 (diagnostic): clock64 stamps of CTA trace_cta, [4][kTrace]
   int trace_cta;
-  int prefetch;                // tiles prefetched into L2 ahead of the smem ring (0 = off)
 };
 constexpr int kTrace = 128;
+constexpr int kSlots = 15;        // trace slots: qk_issue, pv_issue, s_ready, p_done, qk_issued, pv_issued,
+                                  // then p_done of each softmax warp 4..11, then the producer's TMA issue
 #define TRACE(slot, gg)                                                                  \
   do {                                                                                   \
-    if (MODE == 2 && blockIdx.x == a.trace_cta && (gg) < kTrace) a.trace[(slot) * kTrace + (gg)] = clock64(); \
+    if ((MODE & 2) && blockIdx.x == a.trace_cta && (gg) < kTrace) a.trace[(slot) * kTrace + (gg)] = clock64(); \
   } while (0)
 
 template <int W_LAT>
@@ -125,6 +124,9 @@ __device__ __forceinline__ int upper_bound_cum(const int* cum, int n, int x) {  
 
 // MODE 0: the kernel.  MODE 1 (diagnostic, TPLA_K3_MODE=stream): the TMA ring alone — every
 // tile is released as soon as it lands, no MMA/softmax — to measure the cache streaming rate.
+// MODE bit 2 (trace): per-tile clock64 stamps.  Bit 8 (nold): softmax without its TMEM
+// loads/stores.  Bit 4 (notma): no cache loads (stale smem), to time MMA + softmax alone.  Diagnostic modes
+// compute garbage; they exist to isolate the pipeline's limiter.
 template <int W_LAT, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
@@ -197,7 +199,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (MODE == 2 && tid == 0) a.trace[4 * kTrace + 2 * c] = globaltimer();
+  if ((MODE & 2) && tid == 0) a.trace[kSlots * kTrace + 2 * c] = globaltimer();
   const uint32_t tb = tmem_base;
   Sched S;
   S.lo = lo_arr[c];
@@ -209,40 +211,37 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
 
   if (warp == 0) {
     // ============================================================ TMA producer (converged warp, one issuer)
-    // Tile t of the flattened list -> cache row of its first token.  Tiles kPrefetch ahead are
-    // prefetched into L2 so that HBM requests stay in flight while the smem stages are held by
-    // QK -> softmax -> PV (stage hold time, not HBM, would otherwise set the streaming rate).
-    int b_ld = S.b_first, b_pf = S.b_first;
-    auto row_of = [&](int t, int& bb) {
-      while (cum[bb + 1] <= t) ++bb;
-      const int tok = (t - cum[bb]) * kTile;
-      const int page = a.block_table[(long)bb * a.max_pages + tok / a.page_size];
-      return page * a.page_size + tok % a.page_size;
+    // Tile t of the flattened list -> cache row of its first token (a tile never straddles a
+    // page: page_size % 64 == 0).  The page-table lookups are dependent global loads; done one
+    // tile at a time they paced the producer at ~800 cycles per tile (measured: the W = 128
+    // shapes were producer-bound).  Each lane resolves one of the next 32 tiles, a batch ahead,
+    // so the lookup latency is paid once per 32 tiles and hidden behind the previous batch.
+    auto lookup = [&](int tt) {
+      if (tt >= S.hi) return 0;
+      const int bb = upper_bound_cum(cum, a.B + 1, tt) - 1;
+      const int tok = (tt - cum[bb]) * kTile;
+      return a.block_table[(long)bb * a.max_pages + tok / a.page_size] * a.page_size + tok % a.page_size;
     };
-    const int kPrefetch = a.prefetch;
-    for (int t = S.lo; kPrefetch > 0 && t < min(S.hi, S.lo + kPrefetch); ++t) {
-      const int row = row_of(t, b_pf);
-      if (elect_one()) {
-#pragma unroll
-        for (int j = 0; j < C::NBOX; ++j) tma_prefetch_2d(&tmap, j * 64, row);
-      }
-      __syncwarp();
-    }
+    int rows_cur = lookup(S.lo + lane), rows_next = lookup(S.lo + 32 + lane);
     for (int t = S.lo, g = 0; t < S.hi; ++t, ++g) {
+      if (g > 0 && (g & 31) == 0) {
+        rows_cur = rows_next;
+        rows_next = lookup(t + 32 + lane);
+      }
+      const int row = __shfl_sync(0xffffffffu, rows_cur, g & 31);
       const int st = g % C::NST;
       mbar_wait(&kv_empty[st], ((g / C::NST) & 1) ^ 1);
-      const int row_pf = (kPrefetch > 0 && t + kPrefetch < S.hi) ? row_of(t + kPrefetch, b_pf) : -1;
-      const int row = row_of(t, b_ld);
       if (elect_one()) {
-        if (row_pf >= 0) {
-#pragma unroll
-          for (int j = 0; j < C::NBOX; ++j) tma_prefetch_2d(&tmap, j * 64, row_pf);
-        }
+        TRACE(14, g);
         uint8_t* dst = s_kv + st * C::STAGE_BYTES;
-        mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
+        if (MODE & 4) {
+          mbar_arrive(&kv_full[st]);      // diagnostic: no HBM traffic, stale smem contents
+        } else {
+          mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
 #pragma unroll
-        for (int j = 0; j < C::NBOX; ++j)
-          tma_load_2d(dst + j * C::BOX_BYTES, &tmap, j * 64, row, &kv_full[st], kEvictFirst);
+          for (int j = 0; j < C::NBOX; ++j)
+            tma_load_2d(dst + j * C::BOX_BYTES, &tmap, j * 64, row, &kv_full[st], kEvictFirst);
+        }
       }
       __syncwarp();
     }
@@ -285,6 +284,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
                  (first_pv && kk == 0) ? 0u : 1u);
         mma_commit(&kv_empty[st]);
         mma_commit(&pv_done[gp & 1]);
+        TRACE(5, gp);
       }
       __syncwarp();
     };
@@ -309,6 +309,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
             mma_ss(s_tmem, qpe_desc + uint64_t(kk * 2),
                    kv_desc + uint64_t(((C::NBOX - 1) * C::BOX_BYTES + kk * 32) >> 4), id_qk, 1u);
           mma_commit(&s_full[g & 1]);
+          TRACE(4, g);
         }
         __syncwarp();
         if (t > t0) issue_pv(g - 1, t - 1 == t0);
@@ -370,8 +371,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         if (warp == 4 && lane == 0) TRACE(2, g);
         tc_fence_after();
         uint32_t sv[32];
-        tmem_ld32(lane_base + C::S_COL0 + sb * kTile + 32 * half, sv);
-        tmem_ld_wait();
+        if (MODE & 8) {                                 // diagnostic: no TMEM traffic in softmax
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sv[j] = __float_as_uint(float((lane * 7 + j * 3 + g) & 15));
+        } else {
+          tmem_ld32(lane_base + C::S_COL0 + sb * kTile + 32 * half, sv);
+          tmem_ld_wait();
+        }
         float* x = reinterpret_cast<float*>(sv);        // raw logits (sm_scale not applied yet)
         const int nvalid = S_b - (t - cum[b]) * kTile - 32 * half;
         if (nvalid < 32) {                               // ragged last tile of the sequence
@@ -422,10 +428,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           pw[j + 1] = pack_bf16x2(p2, p3);
         }
         // P (bf16 pairs) over columns [16*half, 16*half+16) of S(g): tokens 32*half .. +31
-        tmem_st16(lane_base + C::S_COL0 + sb * kTile + 16 * half, pw);
+        if (MODE & 8) {
+          if (pw[0] == 0x7fc00001u) tmem_st16(lane_base + C::S_COL0 + sb * kTile + 16 * half, pw);  // keep the math
+        } else {
+          tmem_st16(lane_base + C::S_COL0 + sb * kTile + 16 * half, pw);
+        }
         tmem_st_wait();
         tc_fence_before();
         if (warp == 4 && lane == 0) TRACE(3, g);
+        if (lane == 0) TRACE(6 + warp - 4, g);
         mbar_arrive(&p_full[sb]);
       }
       // The segment's QKs are all complete (its last S was just consumed): stage the next
@@ -471,7 +482,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (MODE == 2 && tid == 0) a.trace[4 * kTrace + 2 * c + 1] = globaltimer();
+  if ((MODE & 2) && tid == 0) a.trace[kSlots * kTrace + 2 * c + 1] = globaltimer();
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tb);
 }
 
@@ -557,33 +568,46 @@ template <int W_LAT>
 cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaStream_t s) {
   static const char* mode = getenv("TPLA_K3_MODE");
   if (mode && strcmp(mode, "stream") == 0) return launch_tc_mode<W_LAT, 1>(map, a, n_cta, s);
-  if (mode && strcmp(mode, "trace") == 0) {
+  if (mode && strcmp(mode, "nold") == 0) return launch_tc_mode<W_LAT, 8>(map, a, n_cta, s);
+  if (mode && strcmp(mode, "notma") == 0) return launch_tc_mode<W_LAT, 4>(map, a, n_cta, s);
+  if (mode && strncmp(mode, "trace", 5) == 0) {   // trace, trace_notma, trace_nold
     static long long* buf = nullptr;
-    const int nb = 4 * kTrace + 2 * n_cta;
-    if (!buf) cudaMalloc(&buf, (4 * kTrace + 2 * 1024) * sizeof(long long));
+    const int nb = kSlots * kTrace + 2 * n_cta;
+    if (!buf) cudaMalloc(&buf, (kSlots * kTrace + 2 * kMaxCta) * sizeof(long long));
     TcArgs b = a;
     b.trace = buf;
     const char* tc = getenv("TPLA_K3_TRACE_CTA");
     b.trace_cta = tc ? atoi(tc) : 0;
-    cudaError_t e = launch_tc_mode<W_LAT, 2>(map, b, n_cta, s);
-    static long long h[4 * kTrace + 2 * 1024];
+    cudaError_t e = strcmp(mode, "trace_notma") == 0 ? launch_tc_mode<W_LAT, 6>(map, b, n_cta, s)
+                    : strcmp(mode, "trace_nold") == 0  ? launch_tc_mode<W_LAT, 10>(map, b, n_cta, s)
+                                                        : launch_tc_mode<W_LAT, 2>(map, b, n_cta, s);
+    static long long h[kSlots * kTrace + 2 * kMaxCta];
     cudaStreamSynchronize(s);
     cudaMemcpy(h, buf, nb * sizeof(long long), cudaMemcpyDeviceToHost);
-    long long t0 = h[4 * kTrace], t1 = 0, s_max = 0;
+    const long long* cs = h + kSlots * kTrace;
+    long long t0 = cs[0], t1 = 0, s_max = 0;
     for (int c = 0; c < n_cta; ++c) {
-      t0 = std::min(t0, h[4 * kTrace + 2 * c]);
-      t1 = std::max(t1, h[4 * kTrace + 2 * c + 1]);
+      t0 = std::min(t0, cs[2 * c]);
+      t1 = std::max(t1, cs[2 * c + 1]);
     }
     for (int c = 0; c < n_cta; ++c) {
-      long long st = h[4 * kTrace + 2 * c] - t0, en = h[4 * kTrace + 2 * c + 1] - t0;
+      long long st = cs[2 * c] - t0, en = cs[2 * c + 1] - t0;
       s_max = std::max(s_max, st);
       if (c % 8 == 0) fprintf(stderr, "[k3 cta] %3d start %6lld ns end %6lld ns\n", c, st, en);
     }
     fprintf(stderr, "[k3 cta] span %lld ns, latest start %lld ns\n", t1 - t0, s_max);
-    fprintf(stderr, "[k3 trace] g qk_issue pv_issue(g) s_ready(g) p_done(g) (cycles rel. to qk_issue[0])\n");
+    fprintf(stderr, "[k3 trace] g qk_issue qk_issued s_ready p_done pv_issue pv_issued (cycles rel. to qk_issue[0])\n");
     for (int g = 0; g < kTrace; ++g)
-      fprintf(stderr, "[k3 trace] %2d %8lld %8lld %8lld %8lld\n", g, h[g] - h[0], h[kTrace + g] - h[0],
-              h[2 * kTrace + g] - h[0], h[3 * kTrace + g] - h[0]);
+      fprintf(stderr, "[k3 trace] %3d %8lld %8lld %8lld %8lld %8lld %8lld\n", g, h[g] - h[0], h[4 * kTrace + g] - h[0],
+              h[2 * kTrace + g] - h[0], h[3 * kTrace + g] - h[0], h[kTrace + g] - h[0], h[5 * kTrace + g] - h[0]);
+    fprintf(stderr, "[k3 tma] g tma_issue qk_issue (rel. to qk_issue[0])\n");
+    for (int g = 0; g < kTrace; ++g) fprintf(stderr, "[k3 tma] %3d %8lld %8lld\n", g, h[14 * kTrace + g] - h[0], h[g] - h[0]);
+    fprintf(stderr, "[k3 warps] g p_done of softmax warps 4..11 relative to warp 4\n");
+    for (int g = 0; g < kTrace; ++g) {
+      fprintf(stderr, "[k3 warps] %3d", g);
+      for (int w = 0; w < 8; ++w) fprintf(stderr, " %6lld", h[(6 + w) * kTrace + g] - h[6 * kTrace + g]);
+      fprintf(stderr, "\n");
+    }
     return e;
   }
   return launch_tc_mode<W_LAT, 0>(map, a, n_cta, s);
@@ -622,8 +646,6 @@ cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const 
   a.cap = cache.max_pages_per_seq * cache.page_size;
   a.trace = nullptr;
   a.trace_cta = 0;
-  static const char* pf = getenv("TPLA_K3_PREFETCH");
-  a.prefetch = pf ? atoi(pf) : 0;
   switch (g.w_lat) {
     case 64: return launch_tc<64>(map, a, n_cta, s);
     case 128: return launch_tc<128>(map, a, n_cta, s);

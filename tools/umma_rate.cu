@@ -80,6 +80,76 @@ void run(const char* name, int n_cta) {
   cudaFree(d);
 }
 
+
+// K3-like per-tile issue sequence: QK = NQ TS (K-major, N=64) + 4 SS (N=64) into S, commit;
+// PV = 4 TS (MN-major, N=NPV) into O, COMMITS commits.  Reports cycles per tile.
+template <int NQ, int NPV, int COMMITS, int FENCE = 0>
+__global__ void tile_kernel(long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar[4];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 65536 / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1); fence_barrier_init(); }
+  if (warp == 0) tmem_alloc<512>(&tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tmem_base;
+  constexpr int kTiles = 512;
+  if (warp == 1) {
+    constexpr uint32_t id_qk = idesc_bf16(128, 64, false, false);
+    constexpr uint32_t id_pv = idesc_bf16(128, NPV, false, true);
+    constexpr uint32_t hi = desc_sw128_hi(1024);
+    const uint64_t da = make_desc(smem_addr(smem), 16, hi);
+    const uint64_t db = make_desc(smem_addr(smem + 16384), 16, hi);
+    const uint64_t dv = make_desc(smem_addr(smem + 16384), 8192, hi);
+    long long t0 = 0;
+    if (elect_one()) {
+      t0 = clock64();
+      for (int it = 0; it < kTiles; ++it) {
+        const uint32_t s_t = tb + 256 + (it & 1) * 64;   // S double buffer (cols 256..383)
+        if (FENCE & 1) tc_fence_after();
+        if (FENCE & 4) { mbar_wait(&bar[3], 1); tc_fence_after(); }   // completed-phase wait (returns at once)
+        if (FENCE & 8) mbar_wait(&bar[3], 1);
+        for (int kk = 0; kk < NQ; ++kk) mma_ts(s_t, tb + 384 + (kk & 7) * 8, db + uint64_t(kk * 2), id_qk, kk > 0);
+        for (int kk = 0; kk < 4; ++kk) mma_ss(s_t, da + uint64_t(kk * 2), db + uint64_t(kk * 2), id_qk, 1u);
+        if (COMMITS > 0) mma_commit(&bar[0]);
+        if (FENCE & 2) tc_fence_after();
+        for (int kk = 0; kk < 4; ++kk) mma_ts(tb, tb + 448 + kk * 8, dv + uint64_t(kk * 128), id_pv, 1u);
+        if (COMMITS > 1) { mma_commit(&bar[1]); mma_commit(&bar[2]); }
+      }
+      mma_commit(&bar[3]);     // completes after every MMA issued before it
+    }
+    __syncwarp();
+    mbar_wait(&bar[3], 0);
+    if (elect_one()) cyc[blockIdx.x] = (clock64() - t0) / kTiles;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<512>(tb);
+}
+
+template <int NQ, int NPV, int COMMITS, int FENCE = 0>
+void run_tile(const char* name) {
+  long long* d;
+  cudaMalloc(&d, 148 * sizeof(long long));
+  auto k = tile_kernel<NQ, NPV, COMMITS, FENCE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024 + 1024);
+  k<<<148, 128, 66 * 1024 + 1024>>>(d);
+  cudaError_t err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(err)); exit(1); }
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 148; ++i) avg += h[i];
+  printf("%-34s %6.0f cyc/tile (floor %d)\n", name, avg / 148, NQ * 32 + 4 * 48 + 4 * (128 * NPV / 256));
+  cudaFree(d);
+}
+
 int main() {
   int n = 148;
   run<64, false, false>("SS K-major", n);
@@ -92,6 +162,18 @@ int main() {
   run<128, true, true>("TS MN-major", n);
   run<64, true, false>("TS K-major 1 CTA", 1);
   run<256, true, true>("TS MN-major 1 CTA", 1);
+  run_tile<4, 64, 0>("tile c3-like, no commits");
+  run_tile<4, 64, 1>("tile c3-like, 1 commit");
+  run_tile<4, 64, 2>("tile c3-like, 3 commits");
+  run_tile<16, 256, 0>("tile c1-like, no commits");
+  run_tile<16, 256, 2>("tile c1-like, 3 commits");
+  run_tile<4, 64, 2, 1>("tile c3-like, fence before QK");
+  run_tile<4, 64, 2, 3>("tile c3-like, fence before QK+PV");
+  run_tile<4, 64, 2, 4>("tile c3-like, mbar wait+fence");
+  run_tile<16, 256, 2, 3>("tile c1-like, fence before QK+PV");
+  run_tile<4, 64, 2, 8>("tile c3-like, mbar wait only");
+  run_tile<16, 256, 2, 4>("tile c1-like, mbar wait+fence");
+  run_tile<16, 256, 2, 8>("tile c1-like, mbar wait only");
   printf("RATE OK\n");
   return 0;
 }
