@@ -108,7 +108,10 @@ typedef struct tpla_weights {
 /* Paged latent cache of one device: bf16 [num_pages, page_size, row_stride]; a token's row
  * holds [ĉ_j (W_lat) ‖ k^PE (d_r)] in columns [0, W) and zero padding up to row_stride.
  * Token t of sequence b lives in page block_table[b·max_pages_per_seq + t / page_size],
- * row t % page_size.  page_size is a multiple of 64; row_stride a multiple of 64 ≥ W. */
+ * row t % page_size.  page_size is a multiple of 64; row_stride a multiple of 64 ≥ W.
+ * Decode reads whole 64-row groups: rows of a sequence's last 64-row group beyond its length
+ * are multiplied by a zero probability, so they must hold finite values (allocate pages
+ * zero-filled, as the Python runtime does); their contents never reach the output. */
 typedef struct tpla_cache {
   void* base;                  /* device bf16                                  */
   const int32_t* block_table;  /* device int32 [batch, max_pages_per_seq]      */

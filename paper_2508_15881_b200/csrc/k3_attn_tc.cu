@@ -43,7 +43,7 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kTile = 64;         // tokens per tile
+constexpr int kSub = 64;          // cache rows per TMA box (page_size is a multiple of 64)
 constexpr int kThreads = 384;    // w0 TMA, w1 MMA, w2 TMEM alloc, w3 schedule, w4-w11 softmax
 constexpr int kMaxB = 512;        // sequences per launch supported by the smem schedule
 constexpr int kMaxCta = 256;      // persistent grid bound (<= #SMs in practice)
@@ -64,8 +64,9 @@ struct TcArgs {
   int trace_cta;
 };
 constexpr int kTrace = 128;
-constexpr int kSlots = 15;        // trace slots: qk_issue, pv_issue, s_ready, p_done, qk_issued, pv_issued,
-                                  // then p_done of each softmax warp 4..11, then the producer's TMA issue
+constexpr int kSlots = 19;        // trace slots: qk_issue, pv_issue, s_ready, p_done, qk_issued, pv_issued,
+                                  // then p_done of each softmax warp 4..11, then the producer's TMA issue,
+                                  // then warp 4's softmax phases: S loaded, max exchanged, exps done
 #define TRACE(slot, gg)                                                                  \
   do {                                                                                   \
     if ((MODE & 2) && blockIdx.x == a.trace_cta && (gg) < kTrace) a.trace[(slot) * kTrace + (gg)] = clock64(); \
@@ -73,9 +74,18 @@ constexpr int kSlots = 15;        // trace slots: qk_issue, pv_issue, s_ready, p
 
 template <int W_LAT>
 struct Cfg {
+  // Tokens per tile: 128 when the TMEM budget allows it (O, Q' and two 128-column S buffers),
+  // else 64.  Per tile the MMA warp waits on two mbarriers and the softmax warps synchronise
+  // once; at W_lat <= 128 the MMA work per 64-token tile is too short to hide those (measured),
+  // so the larger tile halves the synchronisation per byte.
+  static constexpr int TT = W_LAT <= 128 ? 128 : 64;
+  static constexpr int SUB = TT / kSub;               // TMA boxes per column group per tile
+  static constexpr int CH = TT / 2;                   // S columns per softmax warp
+  static constexpr int SEQ_COST = 512 / TT;           // per-sequence header cost in tiles (schedule)
   static constexpr int W = W_LAT + 64;
-  static constexpr int NBOX = W / 64;                 // 64-column TMA boxes per tile
-  static constexpr int BOX_BYTES = kTile * 128;       // 8 KB
+  static constexpr int NBOX = W / 64;                 // 64-column groups per tile
+  static constexpr int SUB_BYTES = kSub * 128;        // one TMA box: 64 rows x 128 B
+  static constexpr int BOX_BYTES = TT * 128;          // one column group of the tile (TT rows)
   static constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
   static constexpr int QPE_BYTES = 128 * 128;         // q^PE A operand [128 rows x 64] bf16
   static constexpr int NST = std::min(8, (220 * 1024 - QPE_BYTES) / STAGE_BYTES);
@@ -84,7 +94,7 @@ struct Cfg {
   static constexpr int O_COL = 0;
   static constexpr int Q_COL = W_LAT;                 // W_lat/2 columns of packed bf16
   static constexpr int S_COL0 = (W_LAT + W_LAT / 2 + 63) / 64 * 64;
-  static constexpr int S_COLS = S_COL0 + 2 * kTile;
+  static constexpr int S_COLS = S_COL0 + 2 * TT;
   static constexpr int TMEM_COLS = S_COLS <= 256 ? 256 : 512;
   static_assert(S_COLS <= 512, "TMEM budget");
 };
@@ -99,7 +109,7 @@ struct Sched {
 // "header" (its Q load, pipeline refill and the previous segment's epilogue) followed by one
 // unit per tile, so a CTA whose range crosses a sequence boundary gets fewer tiles.  tile_of maps
 // a work position to the first tile at or after it.
-constexpr int kSeqCost = 8;
+template <int kSeqCost>
 __device__ __forceinline__ int tile_of(const int* cum, int B, long w) {
   int lo = 0, hi = B + 1;                       // first b with cum[b] + kSeqCost*b > w
   while (lo < hi) {
@@ -140,6 +150,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   __shared__ uint64_t s_full[2], p_full[2], pv_done[2], q_ready;
   __shared__ uint32_t tmem_base;
   __shared__ int cum[kMaxB + 1];
+  __shared__ int slen[kMaxB];            // min(seq_len, capacity) per sequence
   __shared__ int lo_arr[kMaxCta + 1];    // first tile of every CTA's range (+ the end)
   __shared__ int s_before;
   __shared__ float red_max[2][2][128];   // [tile parity][half][row] partial row maxima
@@ -152,8 +163,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap);
     for (int i = 0; i < C::NST; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 256); mbar_init(&pv_done[i], 1); }
-    mbar_init(&q_ready, 256);
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 8); mbar_init(&pv_done[i], 1); }
+    mbar_init(&q_ready, 8);      // p_full / q_ready: one arrival per softmax warp (elected lane)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
@@ -164,7 +175,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     int carry = 0;
     for (int b0 = 0; b0 < a.B; b0 += 32) {
       int b = b0 + lane;
-      int t = b < a.B ? (min(a.seq_lens[b], a.cap) + kTile - 1) / kTile : 0;
+      const int len = b < a.B ? min(a.seq_lens[b], a.cap) : 0;
+      if (b < a.B) slen[b] = len;
+      int t = (len + C::TT - 1) / C::TT;
       int x = t;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -182,8 +195,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   // CTA pays a serial loop over its predecessors (that loop staggered the CTA starts by up to
   // 6.7 us at 148 CTAs).
   {
-    const long Wt = long(cum[a.B]) + long(kSeqCost) * a.B;     // total work units
-    for (int cc = tid; cc <= n_cta; cc += kThreads) lo_arr[cc] = tile_of(cum, a.B, cc * Wt / n_cta);
+    const long Wt = long(cum[a.B]) + long(C::SEQ_COST) * a.B;     // total work units
+    for (int cc = tid; cc <= n_cta; cc += kThreads) lo_arr[cc] = tile_of<C::SEQ_COST>(cum, a.B, cc * Wt / n_cta);
   }
   __syncthreads();
   {
@@ -211,24 +224,31 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
 
   if (warp == 0) {
     // ============================================================ TMA producer (converged warp, one issuer)
-    // Tile t of the flattened list -> cache row of its first token (a tile never straddles a
-    // page: page_size % 64 == 0).  The page-table lookups are dependent global loads; done one
-    // tile at a time they paced the producer at ~800 cycles per tile (measured: the W = 128
-    // shapes were producer-bound).  Each lane resolves one of the next 32 tiles, a batch ahead,
-    // so the lookup latency is paid once per 32 tiles and hidden behind the previous batch.
-    auto lookup = [&](int tt) {
+    // Tile t of the flattened list -> cache rows of its TT/64 boxes (a 64-row box never
+    // straddles a page: page_size % 64 == 0).  The page-table lookups are dependent global loads;
+    // done one tile at a time they paced the producer at ~800 cycles per tile (measured: the
+    // W = 128 shapes were producer-bound).  Each lane resolves one of the next 32 boxes, a batch
+    // ahead, so the lookup latency is paid once per 32 boxes and hidden behind the previous batch.
+    // Boxes wholly past the sequence end re-load the tile's first box (masked in the softmax).
+    auto lookup = [&](int u) {                         // u = box index within this CTA's range
+      const int tt = S.lo + u / C::SUB;
       if (tt >= S.hi) return 0;
       const int bb = upper_bound_cum(cum, a.B + 1, tt) - 1;
-      const int tok = (tt - cum[bb]) * kTile;
+      const int tok0 = (tt - cum[bb]) * C::TT;
+      int tok = tok0 + (u % C::SUB) * kSub;
+      if (tok >= slen[bb]) tok = tok0;
       return a.block_table[(long)bb * a.max_pages + tok / a.page_size] * a.page_size + tok % a.page_size;
     };
-    int rows_cur = lookup(S.lo + lane), rows_next = lookup(S.lo + 32 + lane);
+    int rows_cur = lookup(lane), rows_next = lookup(32 + lane);
     for (int t = S.lo, g = 0; t < S.hi; ++t, ++g) {
-      if (g > 0 && (g & 31) == 0) {
+      const int u0 = g * C::SUB;                       // SUB divides 32: a tile never spans batches
+      if (u0 > 0 && (u0 & 31) == 0) {
         rows_cur = rows_next;
-        rows_next = lookup(t + 32 + lane);
+        rows_next = lookup(u0 + 32 + lane);
       }
-      const int row = __shfl_sync(0xffffffffu, rows_cur, g & 31);
+      int row[C::SUB];
+#pragma unroll
+      for (int r = 0; r < C::SUB; ++r) row[r] = __shfl_sync(0xffffffffu, rows_cur, (u0 + r) & 31);
       const int st = g % C::NST;
       mbar_wait(&kv_empty[st], ((g / C::NST) & 1) ^ 1);
       if (elect_one()) {
@@ -240,7 +260,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
 #pragma unroll
           for (int j = 0; j < C::NBOX; ++j)
-            tma_load_2d(dst + j * C::BOX_BYTES, &tmap, j * 64, row, &kv_full[st], kEvictFirst);
+#pragma unroll
+            for (int r = 0; r < C::SUB; ++r)
+              tma_load_2d(dst + j * C::BOX_BYTES + r * C::SUB_BYTES, &tmap, j * 64, row[r], &kv_full[st], kEvictFirst);
         }
       }
       __syncwarp();
@@ -263,7 +285,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     }
   } else if (warp == 1) {
     // ============================================================ MMA issuer (converged warp, one issuer)
-    constexpr uint32_t id_qk = idesc_bf16(128, kTile, false, false);
+    constexpr uint32_t id_qk = idesc_bf16(128, C::TT, false, false);
     constexpr uint32_t id_pv = idesc_bf16(128, W_LAT, false, true);
     constexpr uint32_t hi_k = desc_sw128_hi(1024);           // K-major: SBO = 1024 B (8-row groups)
     const uint64_t qpe_desc = make_desc(smem_addr(s_qpe), 16, hi_k);
@@ -277,9 +299,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         TRACE(1, gp);
         // V = latent boxes of the tile, MN-major: 64-column atoms one box (8 KB) apart
         const uint64_t v_desc = make_desc(kv0 + st * C::STAGE_BYTES, C::BOX_BYTES, hi_k);
-        const uint32_t p_tmem = tb + C::S_COL0 + (gp & 1) * kTile;
+        const uint32_t p_tmem = tb + C::S_COL0 + (gp & 1) * C::TT;
 #pragma unroll
-        for (int kk = 0; kk < kTile / 16; ++kk)      // 16 tokens (2 KB of rows) per step
+        for (int kk = 0; kk < C::TT / 16; ++kk)      // 16 tokens (2 KB of rows) per step
           mma_ts(tb + C::O_COL, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), id_pv,
                  (first_pv && kk == 0) ? 0u : 1u);
         mma_commit(&kv_empty[st]);
@@ -299,7 +321,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         if (elect_one()) {
           TRACE(0, g);
           const uint64_t kv_desc = make_desc(kv0 + st * C::STAGE_BYTES, 16, hi_k);
-          const uint32_t s_tmem = tb + C::S_COL0 + (g & 1) * kTile;
+          const uint32_t s_tmem = tb + C::S_COL0 + (g & 1) * C::TT;
 #pragma unroll
           for (int kk = 0; kk < W_LAT / 16; ++kk)     // Q'_j (TMEM) x ĉ tileᵀ: box kk/4, +32 B per k-step
             mma_ts(s_tmem, tb + C::Q_COL + kk * 8,
@@ -326,6 +348,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     const int r = q4 * 32 + lane;                       // head row = TMEM lane
     const uint32_t lane_base = tb + (uint32_t(q4 * 32) << 16);
     const bool row_ok = r < a.h_loc;
+    const bool q_active = q4 * 32 < a.h_loc;            // warp-uniform: this quadrant holds heads
     const float sc = a.scale_log2;
     const uint32_t pair_bar = 1 + q4;                   // named barrier of the two warps of a quadrant
     // Q'_j row -> TMEM (A operand, bf16 pairs per 32-bit column), half of it per warp;
@@ -356,43 +379,55 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         fence_proxy_async_smem();
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&q_ready);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&q_ready);
     };
     int g = 0, seg = 0;
     if (S.b_first <= S.b_last) load_q(S.b_first);
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
-      const int S_b = min(a.seq_lens[b], a.cap);
+      const int S_b = slen[b];
       float m_used = -INFINITY;                          // running max, log2 units (same in both halves)
       float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;      // this half's running sum (4 chains)
       for (int t = t0; t < t1; ++t, ++g) {
         const int sb = g & 1;
+        if (warp == 4 && lane == 0) TRACE(18, g);
         mbar_wait(&s_full[sb], (g >> 1) & 1);
         if (warp == 4 && lane == 0) TRACE(2, g);
+        if (!q_active) {                                 // no head rows here: P stays 0 (S rows are 0)
+          if (lane == 0) mbar_arrive(&p_full[sb]);
+          continue;
+        }
         tc_fence_after();
-        uint32_t sv[32];
+        constexpr int CH = C::CH;
+        uint32_t sv[CH / 32][32];
         if (MODE & 8) {                                 // diagnostic: no TMEM traffic in softmax
 #pragma unroll
-          for (int j = 0; j < 32; ++j) sv[j] = __float_as_uint(float((lane * 7 + j * 3 + g) & 15));
+          for (int q = 0; q < CH / 32; ++q)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sv[q][j] = __float_as_uint(float((lane * 7 + j * 3 + g + q) & 15));
         } else {
-          tmem_ld32(lane_base + C::S_COL0 + sb * kTile + 32 * half, sv);
+#pragma unroll
+          for (int q = 0; q < CH / 32; ++q) tmem_ld32(lane_base + C::S_COL0 + sb * C::TT + CH * half + 32 * q, sv[q]);
           tmem_ld_wait();
         }
-        float* x = reinterpret_cast<float*>(sv);        // raw logits (sm_scale not applied yet)
-        const int nvalid = S_b - (t - cum[b]) * kTile - 32 * half;
-        if (nvalid < 32) {                               // ragged last tile of the sequence
+        if (warp == 4 && lane == 0) TRACE(15, g);
+        float* x = reinterpret_cast<float*>(&sv[0][0]); // raw logits (sm_scale not applied yet)
+        const int nvalid = S_b - (t - cum[b]) * C::TT - CH * half;
+        if (nvalid < CH) {                               // ragged last tile of the sequence
 #pragma unroll
-          for (int j = 0; j < 32; ++j) x[j] = j < nvalid ? x[j] : -INFINITY;
+          for (int j = 0; j < CH; ++j) x[j] = j < nvalid ? x[j] : -INFINITY;
         }
         float m0 = x[0], m1 = x[1], m2 = x[2], m3 = x[3];
 #pragma unroll
-        for (int j = 4; j < 32; j += 4) {
+        for (int j = 4; j < CH; j += 4) {
           m0 = fmaxf(m0, x[j]); m1 = fmaxf(m1, x[j + 1]); m2 = fmaxf(m2, x[j + 2]); m3 = fmaxf(m3, x[j + 3]);
         }
         float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
         red_max[sb][half][r] = mx;
         named_bar_sync(pair_bar, 64);
         mx = fmaxf(mx, red_max[sb][half ^ 1][r]) * sc;   // sc > 0: max commutes with scaling
+        if (warp == 4 && lane == 0) TRACE(16, g);
         // Raise the running max only when it grew by more than 2^8 (p stays <= 256 in between).
         // The decision is per row (identical in both halves), but TMEM loads/stores are
         // warp-collective (.sync.aligned), so a warp rescales if any of its rows needs it.
@@ -418,31 +453,35 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           m_used = m_new;
         }
         const float neg_m = -m_used;
-        uint32_t pw[16];
+        uint32_t pw[CH / 2];
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {
+        for (int j = 0; j < CH / 2; j += 2) {
           const float p0 = ex2(fmaf(x[2 * j], sc, neg_m)), p1 = ex2(fmaf(x[2 * j + 1], sc, neg_m));
           const float p2 = ex2(fmaf(x[2 * j + 2], sc, neg_m)), p3 = ex2(fmaf(x[2 * j + 3], sc, neg_m));
           l0 += p0; l1 += p1; l2 += p2; l3 += p3;
           pw[j] = pack_bf16x2(p0, p1);
           pw[j + 1] = pack_bf16x2(p2, p3);
         }
-        // P (bf16 pairs) over columns [16*half, 16*half+16) of S(g): tokens 32*half .. +31
-        if (MODE & 8) {
-          if (pw[0] == 0x7fc00001u) tmem_st16(lane_base + C::S_COL0 + sb * kTile + 16 * half, pw);  // keep the math
-        } else {
-          tmem_st16(lane_base + C::S_COL0 + sb * kTile + 16 * half, pw);
+        if (warp == 4 && lane == 0) TRACE(17, g);
+        // P (bf16 pairs) over columns [CH/2*half, CH/2*(half+1)) of S(g): tokens CH*half .. +CH-1
+        const uint32_t p_addr = lane_base + C::S_COL0 + sb * C::TT + (CH / 2) * half;
+        if (!(MODE & 8) || pw[0] == 0x7fc00001u) {       // (diagnostic nold: keep the math, skip the store)
+          if constexpr (CH == 64) tmem_st32(p_addr, pw);
+          else tmem_st16(p_addr, pw);
         }
         tmem_st_wait();
         tc_fence_before();
         if (warp == 4 && lane == 0) TRACE(3, g);
         if (lane == 0) TRACE(6 + warp - 4, g);
-        mbar_arrive(&p_full[sb]);
+        // one arrival per warp: 32 lane arrivals cost ~350 cycles per tile (measured)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[sb]);
       }
       // The segment's QKs are all complete (its last S was just consumed): stage the next
       // segment's Q now, so its first QKs run on the tensor pipe during this epilogue.  Its
       // first PV still waits for this epilogue: it needs p_full, which these warps signal later.
       if (b < S.b_last) load_q(b + 1);
+      if (!q_active) continue;                          // (both warps of the quadrant skip)
       // ---- epilogue of the segment: unnormalised partial (O, m, l)
       float l = (l0 + l1) + (l2 + l3);
       red_l[half][r] = l;
@@ -602,6 +641,12 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
               h[2 * kTrace + g] - h[0], h[3 * kTrace + g] - h[0], h[kTrace + g] - h[0], h[5 * kTrace + g] - h[0]);
     fprintf(stderr, "[k3 tma] g tma_issue qk_issue (rel. to qk_issue[0])\n");
     for (int g = 0; g < kTrace; ++g) fprintf(stderr, "[k3 tma] %3d %8lld %8lld\n", g, h[14 * kTrace + g] - h[0], h[g] - h[0]);
+    fprintf(stderr, "[k3 phases] g s_ready wait_start ld_done max_done exp_done p_done (warp 4, rel. to s_ready)\n");
+    for (int g = 0; g < kTrace; ++g)
+      fprintf(stderr, "[k3 phases] %3d %8lld %6lld %6lld %6lld %6lld %6lld\n", g, h[2 * kTrace + g] - h[0],
+              h[18 * kTrace + g] - h[2 * kTrace + g],
+              h[15 * kTrace + g] - h[2 * kTrace + g], h[16 * kTrace + g] - h[2 * kTrace + g],
+              h[17 * kTrace + g] - h[2 * kTrace + g], h[3 * kTrace + g] - h[2 * kTrace + g]);
     fprintf(stderr, "[k3 warps] g p_done of softmax warps 4..11 relative to warp 4\n");
     for (int g = 0; g < kTrace; ++g) {
       fprintf(stderr, "[k3 warps] %3d", g);
@@ -620,7 +665,7 @@ bool tc_attention_supported(const Geom& g, int B) {
 }
 
 int tc_num_ctas(int B, int max_seq_len) {
-  long tiles = (long)B * ((max_seq_len + kTile - 1) / kTile);
+  long tiles = (long)B * ((max_seq_len + kSub - 1) / kSub);
   return int(std::max(1L, std::min<long>(std::min(num_sms(), kMaxCta), tiles)));
 }
 
@@ -632,7 +677,7 @@ cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const 
   CUtensorMap map;
   cuuint64_t dims[2] = {cuuint64_t(cache.row_stride), cuuint64_t(cache.num_pages) * cache.page_size};
   cuuint64_t strides[1] = {cuuint64_t(cache.row_stride) * 2};
-  cuuint32_t box[2] = {64, kTile};
+  cuuint32_t box[2] = {64, kSub};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, cache.base, dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

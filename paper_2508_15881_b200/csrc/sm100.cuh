@@ -42,13 +42,33 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return done != 0;
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the phase completes (or
+// the hint expires) instead of re-issuing try_wait in a tight loop
+__device__ __forceinline__ bool mbar_try_wait_suspend(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(smem_addr(bar)), "r"(parity), "r"(hint_ns)
+      : "memory");
+  return done != 0;
+}
 // wait until the phase with the given parity has completed; a pipeline bug traps (the launch
 // fails with an error) instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef TPLA_MBAR_SPIN
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
     if (++spins > (1u << 26)) __trap();
   }
+#else
+  uint32_t tries = 0;
+  while (!mbar_try_wait_suspend(bar, parity, 100000u)) {   // 100 us per attempt
+    if (++tries > (1u << 16)) __trap();
+  }
+#endif
 }
 
 // ------------------------------------------------------------------ proxies / fences

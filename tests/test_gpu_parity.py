@@ -146,10 +146,13 @@ def test_append_rows_match_oracle(dname, kind, mode, g):
 
 
 # ----------------------------------------------------------------------------- K3+K4
-def attention_case(d, dims, g, B, S_list, seed=0, peak=1.0, needle=False, page_perm=None):
+def attention_case(d, dims, g, B, S_list, seed=0, peak=1.0, needle=False, page_perm=None, stale=False):
     k = g
     r = TplaRank(spec_of(dims), k=k, g=g, rank=g - 1, batch=B, max_seq_len=max(S_list), device=d,
                  page_perm_seed=page_perm)
+    if stale:   # finite junk in every row past the lengths: must be masked, never reach O
+        r.cache_buf.copy_(torch.randn(r.cache_buf.shape, generator=torch.Generator(device=d).manual_seed(seed),
+                                      device=d).mul_(300.0).to(torch.bfloat16))
     pl = oplan.make_plan(k, g, dims.h_q, dims.d_c, dims.d_r, g - 1)
     rng = np.random.default_rng(seed)
     rows = []
@@ -193,9 +196,14 @@ def test_attention_parity_small(dname, g):
 
 def test_attention_parity_edge_lengths():
     d = dev()
-    attention_case(d, synth.PRESETS["dsv3"], 2, 6, [1, 63, 64, 65, 128, 129], seed=1)
+    attention_case(d, synth.PRESETS["dsv3"], 2, 6, [1, 63, 64, 65, 128, 129], seed=1, stale=True)
     attention_case(d, synth.PRESETS["dsv3"], 2, 2, [4097, 2000], seed=2, needle=True)
     attention_case(d, synth.PRESETS["dsv3"], 8, 2, [1500, 3], seed=4, peak=3.0)
+    # 128-token tiles (W_lat <= 128): ragged lengths around the 64-row box and 128-row tile edges
+    attention_case(d, synth.PRESETS["dsv3"], 8, 9, [1, 63, 64, 65, 127, 128, 129, 192, 255], seed=7, stale=True)
+    attention_case(d, synth.PRESETS["dsv3"], 4, 5, [64, 65, 191, 193, 256], seed=8, page_perm=5)
+    # 64 heads per device: TMEM lane quadrants 2-3 hold no head rows
+    attention_case(d, synth.PRESETS["kimi"], 4, 4, [1, 64, 129, 640], seed=9)
 
 
 def test_attention_parity_divergent_rescale():
