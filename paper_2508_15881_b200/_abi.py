@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtpla.so")
+# TPLA_LIB: an alternative build of the same library (kernel-variant experiments, tools/build_variant.py)
+LIB_PATH = os.environ.get("TPLA_LIB") or os.path.join(_HERE, "libtpla.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2508_15881_b200.build` "

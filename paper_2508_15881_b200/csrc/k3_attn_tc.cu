@@ -452,16 +452,25 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           }
           m_used = m_new;
         }
-        const float neg_m = -m_used;
+        // Paired fp32 ops (FFMA2 / FADD2: two lanes of work per instruction) for the scale-and-
+        // subtract and the row sums: the loop is issue-bound (measured: moving exponentials from
+        // MUFU to FMA-pipe polynomials made it slower), so every instruction saved counts.
+        const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(-m_used, -m_used);
+        uint64_t l01 = f2_pack(l0, l1), l23 = f2_pack(l2, l3);
         uint32_t pw[CH / 2];
 #pragma unroll
         for (int j = 0; j < CH / 2; j += 2) {
-          const float p0 = ex2(fmaf(x[2 * j], sc, neg_m)), p1 = ex2(fmaf(x[2 * j + 1], sc, neg_m));
-          const float p2 = ex2(fmaf(x[2 * j + 2], sc, neg_m)), p3 = ex2(fmaf(x[2 * j + 3], sc, neg_m));
-          l0 += p0; l1 += p1; l2 += p2; l3 += p3;
+          float y0, y1, y2, y3;
+          f2_unpack(ffma2(f2_pack(x[2 * j], x[2 * j + 1]), sc2, nm2), y0, y1);
+          f2_unpack(ffma2(f2_pack(x[2 * j + 2], x[2 * j + 3]), sc2, nm2), y2, y3);
+          const float p0 = ex2(y0), p1 = ex2(y1), p2 = ex2(y2), p3 = ex2(y3);
+          l01 = fadd2(l01, f2_pack(p0, p1));
+          l23 = fadd2(l23, f2_pack(p2, p3));
           pw[j] = pack_bf16x2(p0, p1);
           pw[j + 1] = pack_bf16x2(p2, p3);
         }
+        f2_unpack(l01, l0, l1);
+        f2_unpack(l23, l2, l3);
         if (warp == 4 && lane == 0) TRACE(17, g);
         // P (bf16 pairs) over columns [CH/2*half, CH/2*(half+1)) of S(g): tokens CH*half .. +CH-1
         const uint32_t p_addr = lane_base + C::S_COL0 + sb * C::TT + (CH / 2) * half;
