@@ -100,8 +100,9 @@ bool wo_tc_supported(int N, int K, int B);
 // W^O is stored blocked [ceil(D/128)][K/64][128][64] when 64 | K (the tcgen05 path), else [D, K]
 inline bool wo_blocked(int K) { return K % 64 == 0; }
 size_t wo_tc_part_bytes(int N, int K, int B);
+// out_bf16 (optional): also write bf16(y) (the step's output when no all-reduce follows)
 cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, void* part_ws, float* y,
-                         bool accumulate, cudaStream_t s);
+                         bool accumulate, uint16_t* out_bf16, cudaStream_t s);
 
 // y[b, n] (=|+=) sum_ks y_part[ks, b, n]
 cudaError_t launch_reduce_slices(const float* y_part, int kslices, int B, int N, float* y, bool accumulate,

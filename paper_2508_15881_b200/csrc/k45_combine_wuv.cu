@@ -13,8 +13,9 @@
 namespace tpla {
 namespace {
 
-constexpr int kThreads = 256;
 constexpr int kMB = 16;     // batch rows per CTA (grid = heads x ceil(B/16))
+constexpr int kThreads = 32 * kMB;   // one warp per row: the merge is load-latency bound, so every
+                                     // row's segment loads are in flight at once
 
 struct FArgs {
   const float* o_part;      // [segs, H_loc, W_lat]
@@ -28,6 +29,7 @@ struct FArgs {
 __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
   pdl_trigger();
   extern __shared__ __align__(128) uint16_t smem[];
+  __shared__ float s_w[kMB][32];                    // per-row segment weights 2^(m_s - M)
   const int h = blockIdx.x;
   const int WP = a.w_lat + 8;                       // padded rows: conflict-free ldmatrix
   uint16_t* sW = smem;                              // [d_h][WP]
@@ -63,15 +65,19 @@ __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
       float L = 0.f;
       for (int s = s0 + lane; s <= s1; s += 32) {
         const float* ml = a.ml_part + ((long)s * a.h_loc + h) * 2;
-        L += exp2f(ml[0] - M) * ml[1];
+        const float w = exp2f(ml[0] - M);
+        if (s - s0 < 32) s_w[warp][s - s0] = w;         // first 32 segment weights, for the merge
+        L += w * ml[1];
       }
+      __syncwarp();
       L = warp_sum(L);
       const float inv = 1.f / L;
       for (int c = lane * 8; c < a.w_lat; c += 256) {
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
+#pragma unroll 8
         for (int s = s0; s <= s1; ++s) {
-          const float wgt = exp2f(a.ml_part[((long)s * a.h_loc + h) * 2] - M);
+          // (lanes past W_lat have left this loop: no warp-collective ops in here)
+          const float wgt = s - s0 < 32 ? s_w[warp][s - s0] : exp2f(a.ml_part[((long)s * a.h_loc + h) * 2] - M);
           const float4* src = reinterpret_cast<const float4*>(a.o_part + ((long)s * a.h_loc + h) * a.w_lat + c);
           const float4 x0 = src[0], x1 = src[1];
           acc[0] += wgt * x0.x; acc[1] += wgt * x0.y; acc[2] += wgt * x0.z; acc[3] += wgt * x0.w;

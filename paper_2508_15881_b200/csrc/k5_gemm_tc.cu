@@ -8,7 +8,9 @@
 // (swap-AB: D[128 x Bp] fp32 in TMEM), so the tensor pipe is idle most of the time.
 // Work split: the (row tile, k-step) list is cut into equal contiguous ranges, one per CTA;
 // a range is one or two row-tile segments whose partial sums go to a workspace buffer, and a
-// small deterministic reduce kernel adds a row tile's (contiguous) segments into y.
+// small deterministic reduce kernel adds a row tile's (contiguous) segments into y (and writes
+// the bf16 output when no all-reduce follows).  The first ring stages' weight blocks are
+// requested before the PDL wait, under the previous kernel's tail.
 //
 // Warp roles (256 threads): w0 TMA, w1 MMA, w2 TMEM allocator, w4-w7 epilogue (TMEM lanes).
 #include <cuda.h>
@@ -75,6 +77,13 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     for (int i = 0; i < C::NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 128); }
     fence_barrier_init();
+    // W^O does not depend on the predecessors: fill the ring's weight halves now, under the
+    // previous kernel's tail (PDL); the v halves follow after the wait
+    for (int i = 0; i < C::NST && lo + i < hi; ++i) {
+      const int u = lo + i;
+      mbar_arrive_expect_tx(&full[i], C::STAGE);
+      tma_load_2d(smem + i * C::STAGE, &mapA, 0, u * kTM, &full[i], kEvictFirst);   // blocked: unit u = block u
+    }
   }
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
   pdl_wait();   // v (and y) come from the predecessors
@@ -89,12 +98,14 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     int g = 0, rt = lo / a.k_steps, ks = lo % a.k_steps;
     for (int u = lo; u < hi; ++u, ++g) {
       const int st = g % C::NST;
-      mbar_wait(&empty[st], ((g / C::NST) & 1) ^ 1);
+      if (g >= C::NST) mbar_wait(&empty[st], ((g / C::NST) & 1) ^ 1);
       if (elect_one()) {
         uint8_t* dst = smem + st * C::STAGE;
-        mbar_arrive_expect_tx(&full[st], C::STAGE);
-        // weights (blocked layout: tile (rt, ks) is one contiguous 16 KB block), read once
-        tma_load_2d(dst, &mapA, 0, (rt * a.k_steps + ks) * kTM, &full[st], kEvictFirst);
+        if (g >= C::NST) {   // (the first NST weight blocks were issued before the PDL wait)
+          mbar_arrive_expect_tx(&full[st], C::STAGE);
+          // weights (blocked layout: tile (rt, ks) is one contiguous 16 KB block), read once
+          tma_load_2d(dst, &mapA, 0, (rt * a.k_steps + ks) * kTM, &full[st], kEvictFirst);
+        }
         tma_load_2d(dst + C::A_BYTES, &mapB, ks * kBK, 0, &full[st], kEvictNormal);    // v: re-read per tile
       }
       __syncwarp();
@@ -166,9 +177,10 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tb);
 }
 
-// y[b, n] = (accumulate ? y[b, n] : 0) + Σ_{seg of tile n/128} part[seg, b, n % 128]   (fixed order)
+// y[b, n] = (accumulate ? y[b, n] : 0) + Σ_{seg of tile n/128} part[seg, b, n % 128]   (fixed order);
+// out (optional): the bf16 copy of y (the final cast, when no all-reduce follows)
 __global__ void reduce_seg_kernel(const float* __restrict__ part, const int32_t* __restrict__ meta, int N, int B,
-                                  float* __restrict__ y, int accumulate) {
+                                  float* __restrict__ y, int accumulate, uint16_t* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
   const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
@@ -177,6 +189,7 @@ __global__ void reduce_seg_kernel(const float* __restrict__ part, const int32_t*
   float acc = accumulate ? y[i] : 0.f;
   for (int s = meta[2 * rt]; s <= meta[2 * rt + 1]; ++s) acc += part[((long)s * B + b) * kTM + (n % kTM)];
   y[i] = acc;
+  if (out) out[i] = f2bf(acc);
 }
 
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -249,7 +262,7 @@ size_t wo_tc_part_bytes(int N, int K, int B) {
 }
 
 cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, void* part_ws, float* y,
-                         bool accumulate, cudaStream_t s) {
+                         bool accumulate, uint16_t* out_bf16, cudaStream_t s) {
   const int n_tiles = (N + kTM - 1) / kTM;
   const int NP = B <= 32 ? 32 : B <= 64 ? 64 : B <= 128 ? 128 : 256;
   CUtensorMap mA, mB;
@@ -271,7 +284,8 @@ cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, in
   if (e != cudaSuccess) return e;
   const long n = long(B) * N;
   KernelScope ks("K5_reduce", s);
-  return launch_k(reduce_seg_kernel, int((n + 255) / 256), 256, 0, s, a.part, a.meta, N, B, y, accumulate ? 1 : 0);
+  return launch_k(reduce_seg_kernel, int((n + 255) / 256), 256, 0, s, a.part, a.meta, N, B, y, accumulate ? 1 : 0,
+                  out_bf16);
 }
 
 }  // namespace tpla

@@ -77,6 +77,7 @@ KernelScope::~KernelScope() {
   static const bool debug_sync = getenv("TPLA_DEBUG_SYNC") != nullptr;
   if (debug_sync) {
     // diagnostic mode: run every launch to completion and name the kernel that faulted
+    if (getenv("TPLA_DEBUG_SYNC")[0] == '2') fprintf(stderr, "[tpla] sync after %s\n", name_);
     cudaError_t e = cudaStreamSynchronize(stream);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) fprintf(stderr, "[tpla] kernel %s failed: %s\n", name_, cudaGetErrorString(e));

@@ -493,6 +493,7 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
   if (!w || !w->W_UK || !w->W_UV || !w->W_O) return fail(TPLA_ERR_INVALID_ARG, "NULL weights");
   if (!q_nope || !y || !ws) return fail(TPLA_ERR_INVALID_ARG, "NULL q_nope/y/ws");
   if (!aligned16(q_nope) || !aligned16(ws) || !aligned16(y)) return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
+  if (out && !aligned16(out)) return fail(TPLA_ERR_INVALID_ARG, "out misaligned");
   // A process may hold several of the k ranks (they accumulate into y before the all-reduce),
   // so the communicator spans k/m processes for some m >= 1.
   if (comm && (g.k % comm->world))
@@ -536,9 +537,13 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
   const bool accumulate = (flags & TPLA_DECODE_ACCUMULATE) != 0;
   const int Kw = g.h_loc * g.d_h;
   const char* force = getenv("TPLA_WO");
+  bool out_done = false;
   if (wo_tc_supported(g.D, Kw, B) && !(force && strcmp(force, "mma") == 0)) {
-    e = launch_wo_tc(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, B, base + L.wo_part, y, accumulate, s);
+    // without an all-reduce the segment reduce also writes the bf16 output (no cast launch)
+    uint16_t* out16 = comm ? nullptr : static_cast<uint16_t*>(out);
+    e = launch_wo_tc(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, B, base + L.wo_part, y, accumulate, out16, s);
     if (e != cudaSuccess) return cuda_fail(e, "K5b W_O (tcgen05)");
+    out_done = out16 != nullptr;
   } else {
     e = launch_skinny_gemm(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, B, L.kslices, y_part, s);
     if (e != cudaSuccess) return cuda_fail(e, "K5b W_O");
@@ -550,8 +555,7 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
     ncclResult_t r = g_nccl.AllReduce(y, y, size_t(B) * g.D, ncclFloat32, ncclSum, comm->comm, s);
     if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
   }
-  if (out) {
-    if (!aligned16(out)) return fail(TPLA_ERR_INVALID_ARG, "out misaligned");
+  if (out && !out_done) {
     e = launch_cast_bf16(y, long(B) * g.D, static_cast<uint16_t*>(out), s);
     if (e != cudaSuccess) return cuda_fail(e, "cast");
   }
