@@ -7,24 +7,24 @@
 //   O_j = Σ_t p_t ĉ_{j,t}
 //
 // Mapping: heads are the MMA M dimension (128 TMEM lanes, one head per lane).
-// Per 64-token tile:
-//   QK  S[128 x 64]   = Q'_j (TMEM, A operand, K = W_lat)  x  ĉ tileᵀ (smem, K-major)     tcgen05 TS
+// Per tile of TT tokens (TT = 128 when W_lat <= 128, else 64):
+//   QK  S[128 x TT]   = Q'_j (TMEM, A operand, K = W_lat)  x  ĉ tileᵀ (smem, K-major)     tcgen05 TS
 //                     + q^PE (smem, A, K = 64)             x  k^PE tileᵀ (smem, K-major)   tcgen05 SS
-//   softmax on 4 warps (thread = head row), exp2 with a lazily-raised running max (the O
-//   accumulator is rescaled only when the max grows by more than 2^8), P written back to
-//   TMEM as bf16 over its own S columns
-//   PV  O[128 x W_lat] += P (TMEM, A, K = 64 tokens)       x  ĉ tile (smem, MN-major)      tcgen05 TS
-// The cache tile [64 tokens x (W_lat + 64)] arrives by TMA (SWIZZLE_128B, 64-column boxes)
-// into a 5-8 stage mbarrier ring; the same smem bytes serve as the K-major B operand of QK
-// and the MN-major B operand of PV, so every cache byte crosses HBM -> SMEM once.
+//   softmax on 8 warps (thread = head row, two warps per TMEM lane quadrant splitting the
+//   columns), exp2 with a lazily-raised running max (the O accumulator is rescaled only when the
+//   max grows by more than 2^8), P written back to TMEM as bf16 over its own S columns
+//   PV  O[128 x W_lat] += P (TMEM, A, K = TT tokens)       x  ĉ tile (smem, MN-major)      tcgen05 TS
+// The cache tile [TT tokens x (W_lat + 64)] arrives by TMA (SWIZZLE_128B, 64-row x 64-column
+// boxes) into a 4-8 stage mbarrier ring; the same smem bytes serve as the K-major B operand of
+// QK and the MN-major B operand of PV, so every cache byte crosses HBM -> SMEM once.
 //
-// Work split: persistent grid (<= #SMs CTAs).  The flattened (sequence, 64-token tile) list is
-// cut into equal contiguous ranges, one per CTA; a range is a few segments (one per sequence
-// it touches).  Each segment leaves an unnormalised partial (O, m, l); K4 merges a sequence's
+// Work split: persistent grid (<= #SMs CTAs).  The flattened (sequence, tile) list is cut into
+// equal contiguous work ranges, one per CTA; a range is a few segments (one per sequence it
+// touches).  Each segment leaves an unnormalised partial (O, m, l); K45 merges a sequence's
 // segments, whose ids are contiguous.
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-// w3 schedule, w4-w7 softmax + Q loader + epilogue (warp w owns TMEM lanes 32*(w%4)..).
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w3 sequence
+// scan, w4-w11 softmax + Q loader + epilogue (warp w owns TMEM lanes 32*(w%4)..).
 #include <cuda.h>
 #include <math.h>
 
@@ -48,6 +48,14 @@ constexpr int kThreads = 384;    // w0 TMA, w1 MMA, w2 TMEM alloc, w3 schedule, 
 constexpr int kMaxB = 512;        // sequences per launch supported by the smem schedule
 constexpr int kMaxCta = 256;      // persistent grid bound (<= #SMs in practice)
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: p <= 2^8 between max updates
+// Every kPolyEvery-th group of 4 exponentials computes 2 of them with ex2_poly2 on the FMA pipe
+// (0 = none).  Measured (tools/gpu_variants.sh): at W_lat <= 128 a 1-in-8 share takes ~3 % off K3
+// (the MUFU-bound exponential phase shrinks); at W_lat = 256 no share helps.
+#ifdef TPLA_POLY_EVERY
+template <int W_LAT> constexpr int kPolyEvery = TPLA_POLY_EVERY;
+#else
+template <int W_LAT> constexpr int kPolyEvery = W_LAT <= 128 ? 2 : 0;
+#endif
 
 struct TcArgs {
   const uint16_t* q_lat;       // [B, H_loc, W_lat]
@@ -453,8 +461,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           m_used = m_new;
         }
         // Paired fp32 ops (FFMA2 / FADD2: two lanes of work per instruction) for the scale-and-
-        // subtract and the row sums: the loop is issue-bound (measured: moving exponentials from
-        // MUFU to FMA-pipe polynomials made it slower), so every instruction saved counts.
+        // subtract and the row sums; the loop is close to both the MUFU and the issue limit, so
+        // only a small share of the exponentials moves to the FMA-pipe polynomial (kPolyEvery).
         const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(-m_used, -m_used);
         uint64_t l01 = f2_pack(l0, l1), l23 = f2_pack(l2, l3);
         uint32_t pw[CH / 2];
@@ -463,7 +471,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           float y0, y1, y2, y3;
           f2_unpack(ffma2(f2_pack(x[2 * j], x[2 * j + 1]), sc2, nm2), y0, y1);
           f2_unpack(ffma2(f2_pack(x[2 * j + 2], x[2 * j + 3]), sc2, nm2), y2, y3);
-          const float p0 = ex2(y0), p1 = ex2(y1), p2 = ex2(y2), p3 = ex2(y3);
+          const float p0 = ex2(y0), p1 = ex2(y1);
+          float p2, p3;
+          if (kPolyEvery<W_LAT> > 0 && (j / 2) % kPolyEvery<W_LAT> == 0) {
+            ex2_poly2(y2, y3, p2, p3);                   // this pair on the FMA pipe (MUFU relief)
+          } else {
+            p2 = ex2(y2);
+            p3 = ex2(y3);
+          }
           l01 = fadd2(l01, f2_pack(p0, p1));
           l23 = fadd2(l23, f2_pack(p2, p3));
           pw[j] = pack_bf16x2(p0, p1);

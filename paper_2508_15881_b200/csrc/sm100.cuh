@@ -256,6 +256,28 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+// (2^x0, 2^x1) without MUFU, on paired FMA-pipe instructions, for x <= 127: x = j + f with
+// j = round(x) from the 1.5·2^23 magic add, f in [-0.5, 0.5], a cubic minimax of 2^f (max rel.
+// error 7.5e-5, far below the bf16 rounding P gets), and j added into the exponent field.
+// x is clamped at -126.5 so that j >= -126: 2^f < 1 has biased exponent 126, and 126 + j must
+// not go negative (below that the result is a denormal ~1e-38, i.e. 0 next to P's 2^-8 floor).
+__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& p0, float& p1) {
+  x0 = fmaxf(x0, -126.5f);
+  x1 = fmaxf(x1, -126.5f);
+  const uint64_t magic = f2_pack(12582912.f, 12582912.f);
+  const uint64_t x = f2_pack(x0, x1);
+  const uint64_t t = fadd2(x, magic);                                  // low mantissa bits: round(x)
+  uint64_t f;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(f) : "l"(x), "l"(fadd2(t, f2_pack(-12582912.f, -12582912.f))));
+  uint64_t p = ffma2(f2_pack(0.05517166f, 0.05517166f), f, f2_pack(0.24261114f, 0.24261114f));
+  p = ffma2(p, f, f2_pack(0.69326097f, 0.69326097f));
+  p = ffma2(p, f, f2_pack(0.99992806f, 0.99992806f));
+  float q0, q1, t0, t1;
+  f2_unpack(p, q0, q1);
+  f2_unpack(t, t0, t1);
+  p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
+  p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
+}
 
 }  // namespace sm100
 }  // namespace tpla
