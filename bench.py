@@ -334,16 +334,17 @@ def main():
         comm = abi.tpla_comm_init(obj[0], N, proc)
     stream = torch.cuda.current_stream()
 
-    def step(i, ck=None, kp=None, q=None, qq=None):
+    def step(i, ck=None, kp=None, q=None, qq=None, o=None):
         ck = new_ck[i % NP] if ck is None else ck
         kp = new_kp[i % NP] if kp is None else kp
         q = qn[i % NP] if q is None else q
         qq = qp[i % NP] if qq is None else qq
+        o = out if o is None else o
         for rk in ranks:
             rk.append(ck, kp, seq_idx, pos_new, abi.RMS_SLICED)
         for j, rk in enumerate(ranks):
             last = j == len(ranks) - 1
-            rk.decode(q, qq, seq_lens, y, out if last else None, accumulate=j > 0, comm=comm if last else None)
+            rk.decode(q, qq, seq_lens, y, o if last else None, accumulate=j > 0, comm=comm if last else None)
 
     def barrier():
         if N > 1:
@@ -481,42 +482,63 @@ def main():
         h_kp = [x.cpu().pin_memory() for x in new_kp]
         h_q = [x.cpu().pin_memory() for x in qn]
         h_qp = [x.cpu().pin_memory() for x in qp]
-        h_out = torch.empty((B, dims.D), dtype=torch.bfloat16).pin_memory()
-        d_ck, d_kp = torch.empty_like(new_ck[0]), torch.empty_like(new_kp[0])
-        d_q, d_qp = torch.empty_like(qn[0]), torch.empty_like(qp[0])
+        # Serving-style pipeline: two input/output buffer sets; step i's host->device copies run on a
+        # copy stream while step i-1 computes, its output comes back on a second copy stream, and
+        # the host consumes step i-1's output (waits for it) after enqueueing step i.
+        h_out = [torch.empty((B, dims.D), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+        d_in = [(torch.empty_like(new_ck[0]), torch.empty_like(new_kp[0]), torch.empty_like(qn[0]),
+                 torch.empty_like(qp[0])) for _ in range(2)]
+        d_out = [torch.empty_like(out) for _ in range(2)]
         h2d = sum(t.numel() * t.element_size() for t in (h_ck[0], h_kp[0], h_q[0], h_qp[0]))
-        d2h = h_out.numel() * h_out.element_size()
+        d2h = h_out[0].numel() * h_out[0].element_size()
         n_e2e = max(10, min(args.steps, 100))
         for i in range(3):
-            step(i, d_ck, d_kp, d_q, d_qp)
-        g1 = None
-        if not args.no_graph:                         # one decode step (K1..K5, C1) as a graph
-            g1 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g1, capture_error_mode="relaxed"):
-                step(0, d_ck, d_kp, d_q, d_qp)
+            step(i, *d_in[i & 1], o=d_out[i & 1])
+        g1 = [None, None]
+        if not args.no_graph:                         # one decode step (K1..K5) per buffer set
+            for s in range(2):
+                g1[s] = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g1[s], capture_error_mode="relaxed"):
+                    step(0, *d_in[s], o=d_out[s])
             stream = torch.cuda.current_stream()
+        cs_in, cs_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_done = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        cs_in.wait_event(e0)
         for i in range(n_e2e):
-            j = i % NP
-            d_ck.copy_(h_ck[j], non_blocking=True)
-            d_kp.copy_(h_kp[j], non_blocking=True)
-            d_q.copy_(h_q[j], non_blocking=True)
-            d_qp.copy_(h_qp[j], non_blocking=True)
-            if g1 is not None:
-                g1.replay()
+            s, j = i & 1, i % NP
+            with torch.cuda.stream(cs_in):
+                if i >= 2:
+                    cs_in.wait_event(ev_done[s])     # buffer set s is free (step i-2 computed)
+                for dst, src in zip(d_in[s], (h_ck[j], h_kp[j], h_q[j], h_qp[j])):
+                    dst.copy_(src, non_blocking=True)
+                ev_in[s].record(cs_in)
+            stream.wait_event(ev_in[s])
+            if g1[s] is not None:
+                g1[s].replay()
             else:
-                step(i, d_ck, d_kp, d_q, d_qp)
-            h_out.copy_(out, non_blocking=True)
-            stream.synchronize()          # the host consumes each step's output before the next
-        e1.record(stream)
+                step(i, *d_in[s], o=d_out[s])
+            ev_done[s].record(stream)
+            with torch.cuda.stream(cs_out):
+                cs_out.wait_event(ev_done[s])
+                h_out[s].copy_(d_out[s], non_blocking=True)
+                ev_out[s].record(cs_out)
+            if i >= 1:
+                ev_out[s ^ 1].synchronize()          # the host consumes step i-1's output
+        ev_out[(n_e2e - 1) & 1].synchronize()
+        e1.record(cs_out)
         torch.cuda.synchronize()
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1))
         e2e = {"value": B * n_e2e / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": n_e2e, "ms_per_step": ems / n_e2e}
+               "d2h_bytes_per_step": d2h, "steps": n_e2e, "ms_per_step": ems / n_e2e,
+               "pipeline": "double-buffered: H2D of step i and D2H of step i-1 on copy streams, "
+                           "overlapping compute; host waits for every step's output"}
 
     cpu = None
     if proc == 0 and N == 1 and not args.no_cpu_baseline:
