@@ -290,6 +290,49 @@ def test_e2e_parity_kimi_shape():
     e2e_case(dev(), synth.PRESETS["kimi"], 4, 4, "hadamard", [64, 129])
 
 
+def test_deterministic_graph_replay_and_fused_bf16_out():
+    """DSV3 shape, k = g = 2 on this GPU: the decode is bitwise deterministic, a CUDA-graph capture
+    of it (PDL launches inside) replays to the same bits, and the bf16 output written by the W^O
+    segment reduce (no all-reduce) is exactly the RNE rounding of y."""
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    k = g = 2
+    S_list = [100, 257, 64]
+    B = len(S_list)
+    w = synth.gen_weights(dims, 5)
+    q, qpe = synth.gen_queries(dims, B, 6)
+    q, qpe = bf16_from_bits(q, d), bf16_from_bits(qpe, d)
+    lens = torch.tensor(S_list, dtype=torch.int32, device=d)
+    ranks = []
+    for rid in range(k):
+        r = TplaRank(spec_of(dims), k=k, g=g, rank=rid, batch=B, max_seq_len=max(S_list), device=d)
+        r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_HADAMARD, sign_seed=9)
+        for b, S in enumerate(S_list):
+            r.prefill(bf16_from_bits(synth.gen_raw_ckv(dims, S, 7, b), d), bf16_from_bits(synth.gen_kpe(dims, S, 7, b), d),
+                      torch.full((S,), b, dtype=torch.int32, device=d), torch.arange(S, dtype=torch.int32, device=d))
+        ranks.append(r)
+
+    def run(y, out):
+        for j, r in enumerate(ranks):
+            r.decode(q, qpe, lens, y, out if j == k - 1 else None, accumulate=j > 0)
+
+    ys = [torch.zeros((B, dims.D), dtype=torch.float32, device=d) for _ in range(3)]
+    outs = [torch.empty((B, dims.D), dtype=torch.bfloat16, device=d) for _ in range(3)]
+    run(ys[0], outs[0])
+    run(ys[1], outs[1])
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+        run(ys[2], outs[2])
+    ys[2].zero_()
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    for i in (1, 2):
+        assert torch.equal(ys[i], ys[0]) and torch.equal(outs[i], outs[0])
+    assert torch.equal(outs[0], ys[0].to(torch.bfloat16))
+    assert torch.isfinite(ys[0]).all() and ys[0].abs().max() > 0
+
+
 def test_bf16_output_and_nccl_world1():
     """tpla_decode with a 1-rank NCCL communicator (the C1 call path) and the bf16 output cast."""
     d = dev()
