@@ -146,10 +146,10 @@ def test_append_rows_match_oracle(dname, kind, mode, g):
 
 
 # ----------------------------------------------------------------------------- K3+K4
-def attention_case(d, dims, g, B, S_list, seed=0, peak=1.0, needle=False, page_perm=None, stale=False):
+def attention_case(d, dims, g, B, S_list, seed=0, peak=1.0, needle=False, page_perm=None, stale=False, page_size=64):
     k = g
     r = TplaRank(spec_of(dims), k=k, g=g, rank=g - 1, batch=B, max_seq_len=max(S_list), device=d,
-                 page_perm_seed=page_perm)
+                 page_perm_seed=page_perm, page_size=page_size)
     if stale:   # finite junk in every row past the lengths: must be masked, never reach O
         r.cache_buf.copy_(torch.randn(r.cache_buf.shape, generator=torch.Generator(device=d).manual_seed(seed),
                                       device=d).mul_(300.0).to(torch.bfloat16))
@@ -204,6 +204,15 @@ def test_attention_parity_edge_lengths():
     attention_case(d, synth.PRESETS["dsv3"], 4, 5, [64, 65, 191, 193, 256], seed=8, page_perm=5)
     # 64 heads per device: TMEM lane quadrants 2-3 hold no head rows
     attention_case(d, synth.PRESETS["kimi"], 4, 4, [1, 64, 129, 640], seed=9)
+
+
+@pytest.mark.parametrize("page_size", [128, 256])
+def test_attention_parity_page_sizes(page_size):
+    """Pages larger than the 64-row TMA box: boxes are looked up individually (64- and 128-token tiles)."""
+    d = dev()
+    for g in (2, 8):
+        attention_case(d, synth.PRESETS["dsv3"], g, 4, [63, 129, 300, 513], seed=10 + g, page_perm=page_size,
+                       page_size=page_size, stale=True)
 
 
 def test_attention_parity_divergent_rescale():
