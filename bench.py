@@ -45,6 +45,14 @@ WORKLOADS = {
                     "batch 64, TPLA g=4", model="kimi", B=64, S=32768, g=4, xform="hadamard"),
     "c3": dict(desc="configs[3]: DeepSeek-V3 decode at 128K context, batch 16, g=8, Hadamard-rotated cache",
                model="dsv3", B=16, S=131072, g=8, xform="hadamard"),
+    # SURVEY §8(d) headline shape: one latent shard per GPU on 8 GPUs (all k=8 shards on one GPU here)
+    "h8": dict(desc="SURVEY 8(d) headline shape: DeepSeek-V3 32K context, batch 32, g=8 (one latent shard per GPU "
+                    "at 8 GPUs)", model="dsv3", B=32, S=32768, g=8, xform="hadamard"),
+    # configs[4] baseline: replicated-MLA cache (g = 1); "mla2" = the paper's MLA TP=2 (heads split)
+    "mla1": dict(desc="configs[4] baseline: MLA (g=1, replicated 576-wide cache), DeepSeek-V3 32K, batch 32, "
+                      "all heads on one rank", model="dsv3", B=32, S=32768, g=1, xform="identity"),
+    "mla2": dict(desc="configs[4] baseline: MLA (g=1) with heads split over k=2 (the paper's MLA TP=2), "
+                      "DeepSeek-V3 32K, batch 32", model="dsv3", B=32, S=32768, g=1, k=2, xform="identity"),
 }
 SEED = 1001   # seed = 1000 + config index
 
@@ -234,7 +242,7 @@ def config_of(wl, N, k, g):
 def run_reference(args):
     wl = WORKLOADS[args.workload]
     N = args.gpus
-    k = max(N, wl["g"])
+    k = max(N, wl.get("k", wl["g"]))
     g = wl["g"]
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -289,7 +297,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     dims = synth.PRESETS[wl["model"]]
     g = wl["g"]
-    k = max(N, g)
+    k = max(N, wl.get("k", g))
     if k % N or dims.h_q % (k // g):
         raise SystemExit(f"k={k} ranks cannot be spread over {N} GPUs")
     m = k // N
@@ -302,7 +310,8 @@ def main():
     ranks = []
     for r in my_ranks:
         rk = TplaRank(spec, k=k, g=g, rank=r, batch=B, max_seq_len=S, device=dev)
-        rk.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_HADAMARD, sign_seed=SEED)
+        xf = abi.XFORM_HADAMARD if wl["xform"] == "hadamard" else abi.XFORM_IDENTITY
+        rk.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=xf, sign_seed=SEED)
         ranks.append(rk)
     del w
     gen = torch.Generator(device=dev)

@@ -78,7 +78,8 @@ cudaError_t launch_combine(const Geom& g, int B, const SplitPlan& sp, const floa
 
 // Blackwell-native K3 (tcgen05/TMEM/TMA, persistent) and its segment combine.
 bool tc_attention_supported(const Geom& g, int B);
-int tc_num_ctas(int B, int max_seq_len);
+// persistent K3 grid in logical CTAs (a logical CTA is a cluster of two for W_lat = 512)
+int tc_num_ctas(const Geom& g, int B, int max_seq_len);
 cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
                                   const int32_t* seq_lens, int B, int n_cta, float* o_part, float* ml_part,
                                   int32_t* meta, cudaStream_t s);

@@ -72,7 +72,7 @@ struct TcArgs {
   int trace_cta;
 };
 constexpr int kTrace = 128;
-constexpr int kSlots = 19;        // trace slots: qk_issue, pv_issue, s_ready, p_done, qk_issued, pv_issued,
+constexpr int kSlots = 22;        // trace slots: qk_issue, pv_issue, s_ready, p_done, qk_issued, pv_issued,
                                   // then p_done of each softmax warp 4..11, then the producer's TMA issue,
                                   // then warp 4's softmax phases: S loaded, max exchanged, exps done
 #define TRACE(slot, gg)                                                                  \
@@ -82,26 +82,34 @@ constexpr int kSlots = 19;        // trace slots: qk_issue, pv_issue, s_ready, p
 
 template <int W_LAT>
 struct Cfg {
+  // PAIR (W_lat = 512: g = 1, plain MLA): O [128 x 512] fp32 alone would fill TMEM, so a cluster of
+  // two CTAs splits the latent: CTA r holds Q'[:, 256r:256r+256], streams latent columns
+  // [256r, 256r+256) (+ the RoPE part), computes partial logits, swaps them with its peer through
+  // distributed shared memory (st.async into the peer's buffer) and sums them — exact logits,
+  // the softmax is then identical in both — and accumulates O[:, 256r:256r+256].
+  static constexpr bool PAIR = W_LAT == 512;
+  static constexpr int WL = PAIR ? 256 : W_LAT;       // latent columns this CTA handles
   // Tokens per tile: 128 when the TMEM budget allows it (O, Q' and two 128-column S buffers),
   // else 64.  Per tile the MMA warp waits on two mbarriers and the softmax warps synchronise
   // once; at W_lat <= 128 the MMA work per 64-token tile is too short to hide those (measured),
   // so the larger tile halves the synchronisation per byte.
-  static constexpr int TT = W_LAT <= 128 ? 128 : 64;
+  static constexpr int TT = WL <= 128 ? 128 : 64;
   static constexpr int SUB = TT / kSub;               // TMA boxes per column group per tile
   static constexpr int CH = TT / 2;                   // S columns per softmax warp
   static constexpr int SEQ_COST = 512 / TT;           // per-sequence header cost in tiles (schedule)
-  static constexpr int W = W_LAT + 64;
-  static constexpr int NBOX = W / 64;                 // 64-column groups per tile
+  static constexpr int W = WL + 64;
+  static constexpr int NBOX = W / 64;                 // 64-column groups per tile (latent part + RoPE)
   static constexpr int SUB_BYTES = kSub * 128;        // one TMA box: 64 rows x 128 B
   static constexpr int BOX_BYTES = TT * 128;          // one column group of the tile (TT rows)
   static constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
   static constexpr int QPE_BYTES = 128 * 128;         // q^PE A operand [128 rows x 64] bf16
-  static constexpr int NST = std::min(8, (220 * 1024 - QPE_BYTES) / STAGE_BYTES);
-  static constexpr int SMEM = 1024 + QPE_BYTES + NST * STAGE_BYTES;
+  static constexpr int XCH_BYTES = PAIR ? 2 * 8 * 32 * CH * 4 : 0;   // PAIR: peer's partial logits + ours to send
+  static constexpr int NST = std::min(8, (220 * 1024 - QPE_BYTES - XCH_BYTES) / STAGE_BYTES);
+  static constexpr int SMEM = 1024 + QPE_BYTES + XCH_BYTES + NST * STAGE_BYTES;
   // TMEM columns
   static constexpr int O_COL = 0;
-  static constexpr int Q_COL = W_LAT;                 // W_lat/2 columns of packed bf16
-  static constexpr int S_COL0 = (W_LAT + W_LAT / 2 + 63) / 64 * 64;
+  static constexpr int Q_COL = WL;                    // WL/2 columns of packed bf16
+  static constexpr int S_COL0 = (WL + WL / 2 + 63) / 64 * 64;
   static constexpr int S_COLS = S_COL0 + 2 * TT;
   static constexpr int TMEM_COLS = S_COLS <= 256 ? 256 : 512;
   static_assert(S_COLS <= 512, "TMEM budget");
@@ -153,7 +161,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* s_qpe = smem;
-  uint8_t* s_kv = smem + C::QPE_BYTES;
+  float* s_xch = reinterpret_cast<float*>(smem + C::QPE_BYTES);   // PAIR: recv [8 warps][CH/4][32 lanes] float4,
+                                                                   // then the send staging buffer (same shape)
+  uint8_t* s_kv = smem + C::QPE_BYTES + C::XCH_BYTES;
   __shared__ uint64_t kv_full[C::NST], kv_empty[C::NST];
   __shared__ uint64_t s_full[2], p_full[2], pv_done[2], q_ready;
   __shared__ uint32_t tmem_base;
@@ -163,9 +173,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   __shared__ int s_before;
   __shared__ float red_max[2][2][128];   // [tile parity][half][row] partial row maxima
   __shared__ float red_l[2][128];        // [half][row] partial row sums at a segment end
+  __shared__ uint64_t x_full[8], x_ok[8]; // PAIR, per softmax warp: peer's logits landed / peer read ours
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int c = blockIdx.x, n_cta = gridDim.x;
+  // PAIR: CTAs 2c and 2c+1 form a cluster and share logical work range c
+  const int c = C::PAIR ? blockIdx.x >> 1 : blockIdx.x, n_cta = C::PAIR ? gridDim.x >> 1 : gridDim.x;
+  const uint32_t crank = C::PAIR ? cluster_ctarank() : 0;            // latent half of this CTA
 
   // ---------------------------------------------------------------- setup
   if (warp == 0 && lane == 0) {
@@ -173,8 +186,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     for (int i = 0; i < C::NST; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 8); mbar_init(&pv_done[i], 1); }
     mbar_init(&q_ready, 8);      // p_full / q_ready: one arrival per softmax warp (elected lane)
+    if (C::PAIR)
+      for (int i = 0; i < 8; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_ok[i], 1); }
     fence_barrier_init();
   }
+  if (C::PAIR) cluster_sync();   // the peer's barriers are initialised before any remote operation
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
   if (tid == 0) s_before = 0;
   pdl_wait();   // everything below reads the predecessors' outputs (seq_lens, Q', cache rows)
@@ -270,7 +286,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           for (int j = 0; j < C::NBOX; ++j)
 #pragma unroll
             for (int r = 0; r < C::SUB; ++r)
-              tma_load_2d(dst + j * C::BOX_BYTES + r * C::SUB_BYTES, &tmap, j * 64, row[r], &kv_full[st], kEvictFirst);
+              tma_load_2d(dst + j * C::BOX_BYTES + r * C::SUB_BYTES, &tmap,
+                          j < C::NBOX - 1 ? int(crank) * C::WL + j * 64 : W_LAT, row[r], &kv_full[st], kEvictFirst);
         }
       }
       __syncwarp();
@@ -294,7 +311,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   } else if (warp == 1) {
     // ============================================================ MMA issuer (converged warp, one issuer)
     constexpr uint32_t id_qk = idesc_bf16(128, C::TT, false, false);
-    constexpr uint32_t id_pv = idesc_bf16(128, W_LAT, false, true);
+    constexpr uint32_t id_pv = idesc_bf16(128, C::WL, false, true);
     constexpr uint32_t hi_k = desc_sw128_hi(1024);           // K-major: SBO = 1024 B (8-row groups)
     const uint64_t qpe_desc = make_desc(smem_addr(s_qpe), 16, hi_k);
     const uint32_t kv0 = smem_addr(s_kv);
@@ -331,11 +348,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           const uint64_t kv_desc = make_desc(kv0 + st * C::STAGE_BYTES, 16, hi_k);
           const uint32_t s_tmem = tb + C::S_COL0 + (g & 1) * C::TT;
 #pragma unroll
-          for (int kk = 0; kk < W_LAT / 16; ++kk)     // Q'_j (TMEM) x ĉ tileᵀ: box kk/4, +32 B per k-step
+          for (int kk = 0; kk < C::WL / 16; ++kk)     // Q'_j (TMEM) x ĉ tileᵀ: box kk/4, +32 B per k-step
             mma_ts(s_tmem, tb + C::Q_COL + kk * 8,
                    kv_desc + uint64_t(((kk >> 2) * C::BOX_BYTES + (kk & 3) * 32) >> 4), id_qk, kk > 0 ? 1u : 0u);
+          // q^PE x k^PE tileᵀ (last box), 4 k-steps of 16; PAIR: each rank takes two of them, so the
+          // partial logits carry half of the RoPE term each and the two QKs take equal time
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)              // q^PE (smem) x k^PE tileᵀ (last box)
+          for (int kk = (C::PAIR ? 2 * int(crank) : 0); kk < (C::PAIR ? 2 * int(crank) + 2 : 4); ++kk)
             mma_ss(s_tmem, qpe_desc + uint64_t(kk * 2),
                    kv_desc + uint64_t(((C::NBOX - 1) * C::BOX_BYTES + kk * 32) >> 4), id_qk, 1u);
           mma_commit(&s_full[g & 1]);
@@ -362,8 +381,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     // Q'_j row -> TMEM (A operand, bf16 pairs per 32-bit column), half of it per warp;
     // q^PE row -> swizzled smem (chunks 4*half .. 4*half+3); then signal the MMA warp
     auto load_q = [&](int bb) {
-        const uint4* src = reinterpret_cast<const uint4*>(a.q_lat + ((long)bb * a.h_loc + r) * W_LAT);
-        constexpr int QC = W_LAT / 2;                   // packed columns of Q'_j
+        const uint4* src = reinterpret_cast<const uint4*>(a.q_lat + ((long)bb * a.h_loc + r) * W_LAT + crank * C::WL);
+        constexpr int QC = C::WL / 2;                   // packed columns of Q'_j
         constexpr int QH = QC / 2 >= 32 ? QC / 2 : 32;  // columns per warp (W_LAT=64: one warp does all)
         const int c_begin = QC / 2 >= 32 ? half * QH : 0;
         if (QC / 2 >= 32 || half == 0) {
@@ -391,6 +410,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         if (lane == 0) mbar_arrive(&q_ready);
     };
     int g = 0, seg = 0;
+    int xk = 0;                                          // PAIR: logit exchanges done by this warp
     if (S.b_first <= S.b_last) load_q(S.b_first);
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
@@ -418,6 +438,48 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
 #pragma unroll
           for (int q = 0; q < CH / 32; ++q) tmem_ld32(lane_base + C::S_COL0 + sb * C::TT + CH * half + 32 * q, sv[q]);
           tmem_ld_wait();
+        }
+        if constexpr (C::PAIR) {
+          // Send this CTA's partial logits (its latent half + half of the RoPE term) into the peer's
+          // buffer, receive the peer's into ours, add: both CTAs then hold the exact logits
+          // (a + b == b + a in fp32, so the two softmaxes are bit-identical).
+          // buffer of this warp: float4 group v of lane l at [v][l] (conflict-free 16-byte accesses)
+          const int xw = warp - 4;
+          float* xb = s_xch + xw * 32 * CH + lane * 4;
+          const uint32_t peer = crank ^ 1u;
+          mbar_wait_poll(&x_ok[xw], (xk & 1) ^ 1);       // the peer consumed our previous send
+          if (warp == 4 && lane == 0) TRACE(19, g);
+          float* xs = xb + 8 * 32 * CH;                    // this warp's send staging buffer
+#pragma unroll
+          for (int q = 0; q < CH / 32; ++q)
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              *reinterpret_cast<uint4*>(xs + (8 * q + v) * 32 * 4) =
+                  make_uint4(sv[q][4 * v], sv[q][4 * v + 1], sv[q][4 * v + 2], sv[q][4 * v + 3]);
+          fence_proxy_async_smem();                        // generic stores -> visible to the bulk copy
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&x_full[xw], 32 * CH * 4);
+            bulk_copy_to_peer(mapa(smem_addr(s_xch + xw * 32 * CH), peer), s_xch + 8 * 32 * CH + xw * 32 * CH,
+                              32 * CH * 4, mapa(smem_addr(&x_full[xw]), peer));
+          }
+          if (warp == 4 && lane == 0) TRACE(20, g);
+          mbar_wait_poll(&x_full[xw], xk & 1);
+          if (warp == 4 && lane == 0) TRACE(21, g);
+#pragma unroll
+          for (int q = 0; q < CH / 32; ++q)
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const float4 o = *reinterpret_cast<const float4*>(xb + (8 * q + v) * 32 * 4);
+              sv[q][4 * v] = __float_as_uint(__uint_as_float(sv[q][4 * v]) + o.x);
+              sv[q][4 * v + 1] = __float_as_uint(__uint_as_float(sv[q][4 * v + 1]) + o.y);
+              sv[q][4 * v + 2] = __float_as_uint(__uint_as_float(sv[q][4 * v + 2]) + o.z);
+              sv[q][4 * v + 3] = __float_as_uint(__uint_as_float(sv[q][4 * v + 3]) + o.w);
+            }
+          __syncwarp();
+          // (relaxed: the buffer's reads above have returned; a release arrive cost ~1500 cycles)
+          if (lane == 0) mbar_arrive_remote_relaxed(mapa(smem_addr(&x_ok[xw]), peer));
+          ++xk;
         }
         if (warp == 4 && lane == 0) TRACE(15, g);
         float* x = reinterpret_cast<float*>(&sv[0][0]); // raw logits (sm_scale not applied yet)
@@ -448,7 +510,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
             mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
-            for (int c0 = half * (W_LAT / 2); c0 < (half + 1) * (W_LAT / 2); c0 += 32) {
+            for (int c0 = half * (C::WL / 2); c0 < (half + 1) * (C::WL / 2); c0 += 32) {
               uint32_t ov[32];
               tmem_ld32(lane_base + C::O_COL + c0, ov);
               tmem_ld_wait();
@@ -515,9 +577,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       l += red_l[half ^ 1][r];
       const int seg_id = S.seg_base + seg;
       {
-        float* op = a.o_part + ((long)seg_id * a.h_loc + r) * W_LAT;
+        float* op = a.o_part + ((long)seg_id * a.h_loc + r) * W_LAT + crank * C::WL;
 #pragma unroll 1
-        for (int c0 = half * (W_LAT / 2); c0 < (half + 1) * (W_LAT / 2); c0 += 32) {
+        for (int c0 = half * (C::WL / 2); c0 < (half + 1) * (C::WL / 2); c0 += 32) {
           uint32_t ov[32];
           tmem_ld32(lane_base + C::O_COL + c0, ov);     // whole warp (.sync.aligned)
           tmem_ld_wait();
@@ -528,15 +590,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
                                                                     __uint_as_float(ov[j + 2]), __uint_as_float(ov[j + 3]));
           }
         }
-        if (row_ok && half == 0) {
+        if (row_ok && half == 0 && crank == 0) {
           a.ml_part[((long)seg_id * a.h_loc + r) * 2] = m_used;
           a.ml_part[((long)seg_id * a.h_loc + r) * 2 + 1] = l;
         }
       }
       // publish the sequence's segment range for K4: the CTA holding its first tile writes the
       // first segment id, the CTA holding its last tile the last one (ids are contiguous)
-      if (r == 0 && half == 0 && t0 == cum[b]) a.meta[2 * b] = seg_id;
-      if (r == 0 && half == 0 && t1 == cum[b + 1]) a.meta[2 * b + 1] = seg_id;
+      if (r == 0 && half == 0 && crank == 0 && t0 == cum[b]) a.meta[2 * b] = seg_id;
+      if (r == 0 && half == 0 && crank == 0 && t1 == cum[b + 1]) a.meta[2 * b + 1] = seg_id;
       named_bar_sync(pair_bar, 64);                     // red_l free again
       tc_fence_before();
     }
@@ -546,6 +608,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   __syncthreads();
   tc_fence_after();
   if ((MODE & 2) && tid == 0) a.trace[kSlots * kTrace + 2 * c + 1] = globaltimer();
+  if (C::PAIR) cluster_sync();   // the peer may still be writing into our smem / arriving on our barriers
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tb);
 }
 
@@ -624,7 +687,9 @@ cudaError_t launch_tc_mode(const CUtensorMap& map, const TcArgs& a, int n_cta, c
     attr = true;
   }
   KernelScope ks(MODE == 0 ? "K3_attn_tc" : "K3_stream_only", s);
-  return launch_k(attn_tc_kernel<W_LAT, MODE>, n_cta, kThreads, C::SMEM, s, map, a);
+  // PAIR: n_cta logical CTAs = n_cta clusters of two
+  return launch_kc(attn_tc_kernel<W_LAT, MODE>, C::PAIR ? 2 : 1, C::PAIR ? 2 * n_cta : n_cta, kThreads, C::SMEM, s,
+                   map, a);
 }
 
 template <int W_LAT>
@@ -665,6 +730,10 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
               h[2 * kTrace + g] - h[0], h[3 * kTrace + g] - h[0], h[kTrace + g] - h[0], h[5 * kTrace + g] - h[0]);
     fprintf(stderr, "[k3 tma] g tma_issue qk_issue (rel. to qk_issue[0])\n");
     for (int g = 0; g < kTrace; ++g) fprintf(stderr, "[k3 tma] %3d %8lld %8lld\n", g, h[14 * kTrace + g] - h[0], h[g] - h[0]);
+    fprintf(stderr, "[k3 xchg] g x_ok sent x_full (warp 4, rel. to s_ready)\n");
+    for (int g = 0; g < kTrace; ++g)
+      fprintf(stderr, "[k3 xchg] %3d %6lld %6lld %6lld\n", g, h[19 * kTrace + g] - h[2 * kTrace + g],
+              h[20 * kTrace + g] - h[2 * kTrace + g], h[21 * kTrace + g] - h[2 * kTrace + g]);
     fprintf(stderr, "[k3 phases] g s_ready wait_start ld_done max_done exp_done p_done (warp 4, rel. to s_ready)\n");
     for (int g = 0; g < kTrace; ++g)
       fprintf(stderr, "[k3 phases] %3d %8lld %6lld %6lld %6lld %6lld %6lld\n", g, h[2 * kTrace + g] - h[0],
@@ -685,12 +754,14 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
 }  // namespace
 
 bool tc_attention_supported(const Geom& g, int B) {
-  return g.d_r == 64 && (g.w_lat == 64 || g.w_lat == 128 || g.w_lat == 256) && g.h_loc <= 128 && B <= kMaxB;
+  return g.d_r == 64 && (g.w_lat == 64 || g.w_lat == 128 || g.w_lat == 256 || g.w_lat == 512) && g.h_loc <= 128 &&
+         B <= kMaxB;
 }
 
-int tc_num_ctas(int B, int max_seq_len) {
+int tc_num_ctas(const Geom& g, int B, int max_seq_len) {
   long tiles = (long)B * ((max_seq_len + kSub - 1) / kSub);
-  return int(std::max(1L, std::min<long>(std::min(num_sms(), kMaxCta), tiles)));
+  const int slots = g.w_lat == 512 ? num_sms() / 2 : num_sms();   // W_lat = 512: CTA pairs
+  return int(std::max(1L, std::min<long>(std::min(slots, kMaxCta), tiles)));
 }
 
 cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
@@ -719,6 +790,7 @@ cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const 
     case 64: return launch_tc<64>(map, a, n_cta, s);
     case 128: return launch_tc<128>(map, a, n_cta, s);
     case 256: return launch_tc<256>(map, a, n_cta, s);
+    case 512: return launch_tc<512>(map, a, n_cta, s);
   }
   return cudaErrorNotSupported;
 }

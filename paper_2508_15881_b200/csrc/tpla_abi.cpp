@@ -85,8 +85,10 @@ tpla_status make_geom(const tpla_config* c, Geom* g) {
 tpla_status check_kernel_shapes(const Geom& g) {
   if (!is_pow2(g.d_c) || g.d_c < 32 || g.d_c > 1024)
     return fail(TPLA_ERR_SHAPE, "d_c=%d: kernels need a power of two in [32, 1024]", g.d_c);
-  if (g.w_lat % 32 || g.w_lat > 256)
-    return fail(TPLA_ERR_UNSUPPORTED, "W_lat=%d: decode kernels support multiples of 32 up to 256", g.w_lat);
+  // W_lat = 512 (g = 1, plain MLA) runs on the tcgen05 kernel's CTA-pair path only (d_r = 64)
+  if (g.w_lat % 32 || (g.w_lat > 256 && !(g.w_lat == 512 && g.d_r == 64)))
+    return fail(TPLA_ERR_UNSUPPORTED, "W_lat=%d: decode kernels support multiples of 32 up to 256, and 512 with d_r=64",
+                g.w_lat);
   if (!(g.d_r == 16 || g.d_r == 64)) return fail(TPLA_ERR_UNSUPPORTED, "d_r=%d: decode kernels support 16 or 64", g.d_r);
   if (g.h_loc > 128) return fail(TPLA_ERR_UNSUPPORTED, "H_loc=%d > 128", g.h_loc);
   if (g.d_h % 16 || g.d_h > 256) return fail(TPLA_ERR_UNSUPPORTED, "d_h=%d: multiple of 16 up to 256", g.d_h);
@@ -209,7 +211,7 @@ WsLayout ws_layout(const Geom& g, int B, int max_seq_len) {
   if (K % (64 * L.kslices)) L.kslices = 1;
   // partial (O, m, l) slots: B*n_split for the fixed split (mma.sync K3), n_cta + B segments
   // for the persistent tcgen05 K3 (each CTA range touches at most one more sequence than it starts in)
-  L.n_cta = tc_num_ctas(B, max_seq_len);
+  L.n_cta = tc_num_ctas(g, B, max_seq_len);
   const size_t parts = std::max(size_t(B) * sp.n_split, size_t(L.n_cta) + B);
   size_t off = 0;
   L.q_lat = off;   off += align256(size_t(B) * g.h_loc * g.w_lat * 2);

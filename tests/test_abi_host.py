@@ -110,9 +110,9 @@ def test_workspace_bytes_monotone():
 
 def test_decode_rejects_before_launch():
     # validation happens before any launch: NULL pointers -> INVALID_ARG, unsupported W_lat -> UNSUPPORTED
-    c = cfg(k=1, g=1)                  # W_lat 512: beyond this build's decode kernels
+    c = cfg(d_c=1024, k=1, g=1)        # W_lat 1024: beyond this build's decode kernels (512 is the CTA-pair path)
     w = abi.tpla_weights(1 << 20, 1 << 20, 1 << 20, None, 0, 1.0, 1.0)
-    cache = abi.tpla_cache(1 << 20, 1 << 20, 16, 64, 4, 576, 2)
+    cache = abi.tpla_cache(1 << 20, 1 << 20, 16, 64, 4, 1088, 2)
     with pytest.raises(abi.TplaError) as ei:
         abi.tpla_decode(c, w, cache, 1 << 20, 1 << 20, 1 << 20, 2, 256, 1 << 20, 1 << 30, 1 << 20)
     assert ei.value.status == abi.ERR_UNSUPPORTED

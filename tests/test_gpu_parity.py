@@ -188,7 +188,8 @@ def dims_scale(dims):
     return 1.0 / np.sqrt(dims.d_h + dims.d_r)
 
 
-@pytest.mark.parametrize("dname,g", [("tiny", 2), ("odd", 2), ("dsv3", 2), ("dsv3", 4), ("dsv3", 8), ("kimi", 4)])
+@pytest.mark.parametrize("dname,g", [("tiny", 2), ("odd", 2), ("dsv3", 1), ("dsv3", 2), ("dsv3", 4), ("dsv3", 8),
+                                     ("kimi", 1), ("kimi", 4)])
 def test_attention_parity_small(dname, g):
     d = dev()
     attention_case(d, synth.PRESETS[dname], g, 3, [1, 77, 300], page_perm=3)
@@ -199,6 +200,9 @@ def test_attention_parity_edge_lengths():
     attention_case(d, synth.PRESETS["dsv3"], 2, 6, [1, 63, 64, 65, 128, 129], seed=1, stale=True)
     attention_case(d, synth.PRESETS["dsv3"], 2, 2, [4097, 2000], seed=2, needle=True)
     attention_case(d, synth.PRESETS["dsv3"], 8, 2, [1500, 3], seed=4, peak=3.0)
+    # g = 1 (plain MLA, CTA pairs exchanging partial logits): ragged, needle, stale rows
+    attention_case(d, synth.PRESETS["dsv3"], 1, 6, [1, 63, 64, 65, 129, 700], seed=12, stale=True)
+    attention_case(d, synth.PRESETS["dsv3"], 1, 2, [2500, 90], seed=13, needle=True)
     # 128-token tiles (W_lat <= 128): ragged lengths around the 64-row box and 128-row tile edges
     attention_case(d, synth.PRESETS["dsv3"], 8, 9, [1, 63, 64, 65, 127, 128, 129, 192, 255], seed=7, stale=True)
     attention_case(d, synth.PRESETS["dsv3"], 4, 5, [64, 65, 191, 193, 256], seed=8, page_perm=5)
@@ -290,7 +294,7 @@ def test_e2e_parity_tiny(dname, k, g, kind):
 
 
 @pytest.mark.parametrize("k,g,kind", [(2, 2, "hadamard"), (2, 2, "pca"), (4, 4, "hadamard"), (8, 8, "hadamard"),
-                                      (4, 2, "identity")])
+                                      (4, 2, "identity"), (1, 1, "identity"), (2, 1, "hadamard")])
 def test_e2e_parity_dsv3_shape(k, g, kind):
     e2e_case(dev(), synth.PRESETS["dsv3"], k, g, kind, [5, 200, 333])
 
