@@ -53,6 +53,10 @@ WORKLOADS = {
                       "all heads on one rank", model="dsv3", B=32, S=32768, g=1, xform="identity"),
     "mla2": dict(desc="configs[4] baseline: MLA (g=1) with heads split over k=2 (the paper's MLA TP=2), "
                       "DeepSeek-V3 32K, batch 32", model="dsv3", B=32, S=32768, g=1, k=2, xform="identity"),
+    # two query tokens per sequence per step (MTP / speculative decode); with Kimi's
+    # 64 heads per device the tokens x heads rows fill the 128-row MMA
+    "c2mtp": dict(desc="SURVEY f3: Kimi-K2 shape, 32K context, batch 64, g=4, 2 query tokens per sequence per step "
+                       "(multi-token decode)", model="kimi", B=64, S=32768, g=4, n_q=2, xform="hadamard"),
 }
 SEED = 1001   # seed = 1000 + config index
 
@@ -234,6 +238,7 @@ def _cpu_name():
 def config_of(wl, N, k, g):
     return {"workload": wl["desc"], "global_batch": wl["B"], "seq_len": wl["S"], "heads": synth.PRESETS[wl["model"]].h_q,
             "latent": 512, "rope": 64, "g": g, "k": k, "ranks_per_gpu": k // N, "transform": wl["xform"],
+            "query_tokens_per_seq": wl.get("n_q", 1),
             "parallelism": f"tpla k={k} g={g} over {N} GPU(s)",
             "l2": "no flush: per-step cache reads (>=0.5 GB) exceed the 126 MB L2",
             "data": "synthetic (seeded bf16; DESIGN.md input recipe)"}
@@ -303,13 +308,14 @@ def main():
     m = k // N
     my_ranks = list(range(proc * m, (proc + 1) * m))
     B, S = wl["B"], wl["S"]
+    nq = wl.get("n_q", 1)                    # query tokens per sequence per step (multi-token decode)
     spec = LayerSpec(dims.h_q, dims.d_c, dims.d_r, dims.d_h, dims.D)
 
     # ---- setup (untimed): weights, converted per rank; cache prefilled through K1 (EXACT rows)
     w = synth.gen_weights(dims, SEED)
     ranks = []
     for r in my_ranks:
-        rk = TplaRank(spec, k=k, g=g, rank=r, batch=B, max_seq_len=S, device=dev)
+        rk = TplaRank(spec, k=k, g=g, rank=r, batch=B, max_seq_len=S, device=dev, n_q=nq)
         xf = abi.XFORM_HADAMARD if wl["xform"] == "hadamard" else abi.XFORM_IDENTITY
         rk.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=xf, sign_seed=SEED)
         ranks.append(rk)
@@ -317,25 +323,26 @@ def main():
     gen = torch.Generator(device=dev)
     gen.manual_seed(SEED)
     sig = torch.tensor(synth.latent_spectrum(dims.d_c, dims.n_outlier), dtype=torch.float32, device=dev)
-    pos_all = torch.arange(S - 1, dtype=torch.int32, device=dev)
+    pos_all = torch.arange(S - nq, dtype=torch.int32, device=dev)
     for b in range(B):
-        ck = (torch.randn((S - 1, dims.d_c), generator=gen, device=dev) * sig).to(torch.bfloat16)
-        kp = torch.randn((S - 1, dims.d_r), generator=gen, device=dev).to(torch.bfloat16)
-        sq = torch.full((S - 1,), b, dtype=torch.int32, device=dev)
+        ck = (torch.randn((S - nq, dims.d_c), generator=gen, device=dev) * sig).to(torch.bfloat16)
+        kp = torch.randn((S - nq, dims.d_r), generator=gen, device=dev).to(torch.bfloat16)
+        sq = torch.full((S - nq,), b, dtype=torch.int32, device=dev)
         for rk in ranks:
             rk.prefill(ck, kp, sq, pos_all)
     del ck, kp, sq, pos_all
     # per-step inputs: new latent row + RoPE key of every sequence at position S-1, queries
     NP = 4
-    new_ck = [(torch.randn((B, dims.d_c), generator=gen, device=dev) * sig).to(torch.bfloat16) for _ in range(NP)]
-    new_kp = [torch.randn((B, dims.d_r), generator=gen, device=dev).to(torch.bfloat16) for _ in range(NP)]
-    qn = [torch.randn((B, dims.h_q, dims.d_h), generator=gen, device=dev).to(torch.bfloat16) for _ in range(NP)]
-    qp = [torch.randn((B, dims.h_q, dims.d_r), generator=gen, device=dev).to(torch.bfloat16) for _ in range(NP)]
-    seq_idx = torch.arange(B, dtype=torch.int32, device=dev)
-    pos_new = torch.full((B,), S - 1, dtype=torch.int32, device=dev)
+    qshape = (B, dims.h_q) if nq == 1 else (B, nq, dims.h_q)
+    new_ck = [(torch.randn((B * nq, dims.d_c), generator=gen, device=dev) * sig).to(torch.bfloat16) for _ in range(NP)]
+    new_kp = [torch.randn((B * nq, dims.d_r), generator=gen, device=dev).to(torch.bfloat16) for _ in range(NP)]
+    qn = [torch.randn(qshape + (dims.d_h,), generator=gen, device=dev).to(torch.bfloat16) for _ in range(NP)]
+    qp = [torch.randn(qshape + (dims.d_r,), generator=gen, device=dev).to(torch.bfloat16) for _ in range(NP)]
+    seq_idx = torch.arange(B, dtype=torch.int32, device=dev).repeat_interleave(nq)
+    pos_new = (S - nq + torch.arange(nq, dtype=torch.int32, device=dev)).repeat(B)
     seq_lens = torch.full((B,), S, dtype=torch.int32, device=dev)
-    y = torch.zeros((B, dims.D), dtype=torch.float32, device=dev)
-    out = torch.empty((B, dims.D), dtype=torch.bfloat16, device=dev)
+    y = torch.zeros((B * nq, dims.D), dtype=torch.float32, device=dev)
+    out = torch.empty((B * nq, dims.D), dtype=torch.bfloat16, device=dev)
     comm = None
     if N > 1:
         obj = [abi.tpla_comm_unique_id() if proc == 0 else None]
@@ -353,7 +360,10 @@ def main():
             rk.append(ck, kp, seq_idx, pos_new, abi.RMS_SLICED)
         for j, rk in enumerate(ranks):
             last = j == len(ranks) - 1
-            rk.decode(q, qq, seq_lens, y, o if last else None, accumulate=j > 0, comm=comm if last else None)
+            if nq == 1:
+                rk.decode(q, qq, seq_lens, y, o if last else None, accumulate=j > 0, comm=comm if last else None)
+            else:
+                rk.decode_mtp(q, qq, seq_lens, y, o if last else None, accumulate=j > 0, comm=comm if last else None)
 
     def barrier():
         if N > 1:
@@ -399,11 +409,12 @@ def main():
         abi.tpla_profile_reset()
         # K3 alone: the attention launches of the K steps (same kernel, same cache, Q' of the
         # same shape), back to back with no event nodes; outer events give its launch duration
-        graph_prof = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph_prof, capture_error_mode="relaxed"):
-            for i in range(args.steps):
-                for j, rk in enumerate(ranks):
-                    rk.decode_attention(k3_q[j], qp[i % NP], seq_lens, None)     # K3 alone
+        graph_prof = torch.cuda.CUDAGraph() if nq == 1 else None     # (K3 alone: single-token only)
+        if graph_prof is not None:
+            with torch.cuda.graph(graph_prof, capture_error_mode="relaxed"):
+                for i in range(args.steps):
+                    for j, rk in enumerate(ranks):
+                        rk.decode_attention(k3_q[j], qp[i % NP], seq_lens, None)     # K3 alone
         stream = torch.cuda.current_stream()
         graph.replay()                                   # untimed warm replay
         torch.cuda.synchronize()
@@ -427,14 +438,15 @@ def main():
         torch.cuda.cudart().cudaProfilerStop()
     barrier()
     ms_prof = None
-    if graph_prof is not None:
-        torch.cuda.synchronize()
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0.record(stream)
-        graph_prof.replay()
-        p1.record(stream)
-        torch.cuda.synchronize()
-        ms_prof = p0.elapsed_time(p1) / (args.steps * len(ranks))   # ms per isolated K3 launch
+    if graph is not None:
+        if graph_prof is not None:
+            torch.cuda.synchronize()
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record(stream)
+            graph_prof.replay()
+            p1.record(stream)
+            torch.cuda.synchronize()
+            ms_prof = p0.elapsed_time(p1) / (args.steps * len(ranks))   # ms per isolated K3 launch
         prof = breakdown                                 # in-step durations (roofline)
     else:
         launches = abi.tpla_launch_count() - n0
@@ -443,7 +455,7 @@ def main():
     abi.tpla_profile_enable(False)
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = ms / args.steps
-    value = B * args.steps / (ms / 1e3)
+    value = B * nq * args.steps / (ms / 1e3)
     abi.tpla_sync(stream.cuda_stream)
 
     # ---- roofline of the dominant kernel (K3 attention), per launch = one rank's shard
@@ -451,7 +463,7 @@ def main():
     k3_name = next((n for n in prof if n.startswith("K3")), None)
     plan0 = ranks[0].plan
     bytes_k3 = B * S * plan0.row_width * 2                       # Σ_b S_b · W · 2
-    flops_k3 = 2 * B * S * plan0.h_loc * (2 * plan0.w_lat + dims.d_r)
+    flops_k3 = 2 * B * nq * S * plan0.h_loc * (2 * plan0.w_lat + dims.d_r)   # (MTP: ~S keys per token)
     k3_ms, k3_n = prof.get(k3_name, (float("nan"), 1))
     k3_avg_s = k3_ms / max(k3_n, 1) / 1e3
     gbs = bytes_k3 / k3_avg_s / 1e9
@@ -494,7 +506,7 @@ def main():
         # Serving-style pipeline: two input/output buffer sets; step i's host->device copies run on a
         # copy stream while step i-1 computes, its output comes back on a second copy stream, and
         # the host consumes step i-1's output (waits for it) after enqueueing step i.
-        h_out = [torch.empty((B, dims.D), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+        h_out = [torch.empty((B * nq, dims.D), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
         d_in = [(torch.empty_like(new_ck[0]), torch.empty_like(new_kp[0]), torch.empty_like(qn[0]),
                  torch.empty_like(qp[0])) for _ in range(2)]
         d_out = [torch.empty_like(out) for _ in range(2)]
@@ -544,7 +556,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1))
-        e2e = {"value": B * n_e2e / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+        e2e = {"value": B * nq * n_e2e / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": n_e2e, "ms_per_step": ems / n_e2e,
                "pipeline": "double-buffered: H2D of step i and D2H of step i-1 on copy streams, "
                            "overlapping compute; host waits for every step's output"}

@@ -200,6 +200,22 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
                         int32_t max_seq_len, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,
                         tpla_comm* comm, void* stream);
 
+/* Multi-token decode (speculative / MTP decoding): n_q query tokens per sequence,
+ * already appended to the cache, decoded in one step.  Token i of sequence b sits at position
+ * seq_lens[b] - n_q + i and attends to the first seq_lens[b] - n_q + 1 + i cached tokens (causal
+ * among the new tokens); otherwise exactly tpla_decode per token.  The heads of all
+ * n_q tokens share the tensor-core M dimension: requires the tcgen05 path and n_q * H_loc <= 128
+ * (else TPLA_ERR_UNSUPPORTED), and seq_lens[b] >= n_q (not checked: device data).
+ *   q_nope: device bf16 [B, n_q, h_q, d_h];  q_pe: device bf16 [B, n_q, h_q, d_r];
+ *   y: device fp32 [B * n_q, D] (row b * n_q + i);  out: device bf16 [B * n_q, D] or NULL;
+ *   ws: tpla_decode_workspace_bytes_mtp(cfg, B, n_q, max_seq_len) bytes.  tpla_decode = n_q 1. */
+tpla_status tpla_decode_workspace_bytes_mtp(const tpla_config* cfg, int32_t B, int32_t n_q, int32_t max_seq_len,
+                                            size_t* bytes);
+tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                            const void* q_nope, const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t n_q,
+                            int32_t max_seq_len, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,
+                            tpla_comm* comm, void* stream);
+
 /* K3 + K4 only (attention of one shard, Eq. tpla_softmax_one_device without W^VO):
  *   q_lat: device bf16 [B, H_loc, W_lat] (= Q'_j, mu_j included); q_pe: device bf16 [B, h_q, d_r]
  *   (all heads); O: device fp32 [B, H_loc, W_lat] = Σ_t p_t ĉ_{j,t};  lse: device fp32 [B, H_loc]

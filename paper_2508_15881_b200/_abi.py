@@ -79,6 +79,9 @@ _SIGS = {
     "tpla_decode_workspace_bytes": ([C.POINTER(tpla_config), _I, _I, C.POINTER(_S)], _I),
     "tpla_decode": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _P, _I, _I, _P,
                      _S, _P, _P, _I, _P, _P], _I),
+    "tpla_decode_workspace_bytes_mtp": ([C.POINTER(tpla_config), _I, _I, _I, C.POINTER(_S)], _I),
+    "tpla_decode_mtp": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _P, _I, _I,
+                         _I, _P, _S, _P, _P, _I, _P, _P], _I),
     "tpla_decode_attention": ([C.POINTER(tpla_config), C.POINTER(tpla_cache), _P, _P, _P, _I, _I, _P, _S, _P, _P,
                                _P], _I),
     "tpla_comm_unique_id": ([_P], _I),
@@ -191,6 +194,20 @@ def tpla_decode(cfg, w, cache, q_nope, q_pe, seq_lens, B, max_seq_len, ws, ws_by
     _check(_lib.tpla_decode(C.byref(cfg), C.byref(w), C.byref(cache), _ptr(q_nope), _ptr(q_pe), _ptr(seq_lens), B,
                             max_seq_len, _ptr(ws), ws_bytes, _ptr(y), _ptr(out), flags, comm, _ptr(stream)),
            "tpla_decode")
+
+
+def tpla_decode_workspace_bytes_mtp(cfg, B, n_q, max_seq_len) -> int:
+    out = _S()
+    _check(_lib.tpla_decode_workspace_bytes_mtp(C.byref(cfg), B, n_q, max_seq_len, C.byref(out)),
+           "tpla_decode_workspace_bytes_mtp")
+    return out.value
+
+
+def tpla_decode_mtp(cfg, w, cache, q_nope, q_pe, seq_lens, B, n_q, max_seq_len, ws, ws_bytes, y, out=None, flags=0,
+                    comm=None, stream=0):
+    _check(_lib.tpla_decode_mtp(C.byref(cfg), C.byref(w), C.byref(cache), _ptr(q_nope), _ptr(q_pe), _ptr(seq_lens), B,
+                                n_q, max_seq_len, _ptr(ws), ws_bytes, _ptr(y), _ptr(out), flags, comm, _ptr(stream)),
+           "tpla_decode_mtp")
 
 
 def tpla_decode_attention(cfg, cache, q_lat, q_pe, seq_lens, B, max_seq_len, ws, ws_bytes, O, lse=None, stream=0):

@@ -55,7 +55,7 @@ struct WsLayout {
 };
 
 SplitPlan choose_split(int B, int max_seq_len);
-WsLayout ws_layout(const Geom& g, int B, int max_seq_len);
+WsLayout ws_layout(const Geom& g, int B, int n_q, int max_seq_len);
 
 // ---- kernels (each returns cudaGetLastError() after launch) ----
 cudaError_t launch_append_kv(const Geom& g, int xform_kind, const float* xform, float alpha_j,
@@ -80,16 +80,17 @@ cudaError_t launch_combine(const Geom& g, int B, const SplitPlan& sp, const floa
 bool tc_attention_supported(const Geom& g, int B);
 // persistent K3 grid in logical CTAs (a logical CTA is a cluster of two for W_lat = 512)
 int tc_num_ctas(const Geom& g, int B, int max_seq_len);
+// n_q query tokens per sequence (multi-token decode): MMA rows = n_q * H_loc <= 128
 cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
-                                  const int32_t* seq_lens, int B, int n_cta, float* o_part, float* ml_part,
+                                  const int32_t* seq_lens, int B, int n_q, int n_cta, float* o_part, float* ml_part,
                                   int32_t* meta, cudaStream_t s);
 cudaError_t launch_combine_seg(const Geom& g, int B, const float* o_part, const float* ml_part, const int32_t* meta,
                                uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s);
 
 // K4 + K5a fused (persistent-K3 partials): v[b, h, :] = combine(partials)[b, h, :] · W^UV'_j[h]ᵀ
 bool combine_wuv_supported(const Geom& g);
-cudaError_t launch_combine_wuv(const Geom& g, int B, const float* o_part, const float* ml_part, const int32_t* meta,
-                               const uint16_t* W_UV, uint16_t* v, cudaStream_t s);
+cudaError_t launch_combine_wuv(const Geom& g, int B, int n_q, const float* o_part, const float* ml_part,
+                               const int32_t* meta, const uint16_t* W_UV, uint16_t* v, cudaStream_t s);
 
 // y_part[ks, b, n] = sum_{k in slice ks} Wt[n, k] * v[b, k]; Wt [N, K] bf16, v [B, K] bf16.
 cudaError_t launch_skinny_gemm(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, int kslices,

@@ -66,6 +66,7 @@ struct TcArgs {
   float* ml_part;              // [max_segs, H_loc, 2]
   int32_t* meta;               // [B, 2]: first segment id, segment count
   int B, h_loc, h_q, head_begin, page_size, max_pages;
+  int n_q;                     // query tokens per sequence (multi-token decode): MMA rows = n_q * h_loc
   int cap;                     // max_pages * page_size: lengths beyond the page table are clamped
   float scale_log2;
   long long* trace;            // MODE 2 (diagnostic): clock64 stamps of CTA trace_cta, [4][kTrace]
@@ -374,14 +375,21 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     const int half = (warp - 4) >> 2;                   // 0 or 1
     const int r = q4 * 32 + lane;                       // head row = TMEM lane
     const uint32_t lane_base = tb + (uint32_t(q4 * 32) << 16);
-    const bool row_ok = r < a.h_loc;
-    const bool q_active = q4 * 32 < a.h_loc;            // warp-uniform: this quadrant holds heads
+    // Multi-token decode (n_q > 1): row r = (token i, head h); token i of sequence b sits
+    // at position S_b - n_q + i and attends to the first S_b - n_q + 1 + i cached tokens (causal
+    // among the new tokens, which are already in the cache).
+    const int n_rows = a.n_q * a.h_loc;
+    const bool row_ok = r < n_rows;
+    const bool q_active = q4 * 32 < n_rows;             // warp-uniform: this quadrant holds rows
+    const int tok_i = row_ok ? r / a.h_loc : 0, head_h = row_ok ? r % a.h_loc : 0;
+    const int len_adj = tok_i + 1 - a.n_q;              // this row's visible length = S_b + len_adj
     const float sc = a.scale_log2;
     const uint32_t pair_bar = 1 + q4;                   // named barrier of the two warps of a quadrant
     // Q'_j row -> TMEM (A operand, bf16 pairs per 32-bit column), half of it per warp;
     // q^PE row -> swizzled smem (chunks 4*half .. 4*half+3); then signal the MMA warp
     auto load_q = [&](int bb) {
-        const uint4* src = reinterpret_cast<const uint4*>(a.q_lat + ((long)bb * a.h_loc + r) * W_LAT + crank * C::WL);
+        const uint4* src = reinterpret_cast<const uint4*>(
+            a.q_lat + (((long)bb * a.n_q + tok_i) * a.h_loc + head_h) * W_LAT + crank * C::WL);
         constexpr int QC = C::WL / 2;                   // packed columns of Q'_j
         constexpr int QH = QC / 2 >= 32 ? QC / 2 : 32;  // columns per warp (W_LAT=64: one warp does all)
         const int c_begin = QC / 2 >= 32 ? half * QH : 0;
@@ -397,7 +405,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
             tmem_st32(lane_base + C::Q_COL + c_begin + c0, w);
           }
         }
-        const uint4* pe = reinterpret_cast<const uint4*>(a.q_pe + ((long)bb * a.h_q + a.head_begin + r) * 64);
+        const uint4* pe = reinterpret_cast<const uint4*>(
+            a.q_pe + (((long)bb * a.n_q + tok_i) * a.h_q + a.head_begin + head_h) * 64);
 #pragma unroll
         for (int ch = 4 * half; ch < 4 * half + 4; ++ch) {
           uint4 u = row_ok ? pe[ch] : make_uint4(0, 0, 0, 0);
@@ -414,7 +423,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     if (S.b_first <= S.b_last) load_q(S.b_first);
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
-      const int S_b = slen[b];
+      const int S_b = slen[b] + len_adj;                 // this row's visible length
       float m_used = -INFINITY;                          // running max, log2 units (same in both halves)
       float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;      // this half's running sum (4 chains)
       for (int t = t0; t < t1; ++t, ++g) {
@@ -483,7 +492,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         }
         if (warp == 4 && lane == 0) TRACE(15, g);
         float* x = reinterpret_cast<float*>(&sv[0][0]); // raw logits (sm_scale not applied yet)
-        const int nvalid = S_b - (t - cum[b]) * C::TT - CH * half;
+        const int nvalid = S_b - (t - cum[b]) * C::TT - CH * half;   // (per row when n_q > 1)
         if (nvalid < CH) {                               // ragged last tile of the sequence
 #pragma unroll
           for (int j = 0; j < CH; ++j) x[j] = j < nvalid ? x[j] : -INFINITY;
@@ -525,7 +534,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         // Paired fp32 ops (FFMA2 / FADD2: two lanes of work per instruction) for the scale-and-
         // subtract and the row sums; the loop is close to both the MUFU and the issue limit, so
         // only a small share of the exponentials moves to the FMA-pipe polynomial (kPolyEvery).
-        const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(-m_used, -m_used);
+        // (a row with no visible token yet keeps m = -inf and must give p = 0, not NaN)
+        const float neg_m = m_used == -INFINITY ? 0.f : -m_used;
+        const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(neg_m, neg_m);
         uint64_t l01 = f2_pack(l0, l1), l23 = f2_pack(l2, l3);
         uint32_t pw[CH / 2];
 #pragma unroll
@@ -577,7 +588,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       l += red_l[half ^ 1][r];
       const int seg_id = S.seg_base + seg;
       {
-        float* op = a.o_part + ((long)seg_id * a.h_loc + r) * W_LAT + crank * C::WL;
+        float* op = a.o_part + ((long)seg_id * n_rows + r) * W_LAT + crank * C::WL;
 #pragma unroll 1
         for (int c0 = half * (C::WL / 2); c0 < (half + 1) * (C::WL / 2); c0 += 32) {
           uint32_t ov[32];
@@ -591,8 +602,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           }
         }
         if (row_ok && half == 0 && crank == 0) {
-          a.ml_part[((long)seg_id * a.h_loc + r) * 2] = m_used;
-          a.ml_part[((long)seg_id * a.h_loc + r) * 2 + 1] = l;
+          a.ml_part[((long)seg_id * n_rows + r) * 2] = m_used;
+          a.ml_part[((long)seg_id * n_rows + r) * 2 + 1] = l;
         }
       }
       // publish the sequence's segment range for K4: the CTA holding its first tile writes the
@@ -765,7 +776,7 @@ int tc_num_ctas(const Geom& g, int B, int max_seq_len) {
 }
 
 cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
-                                  const int32_t* seq_lens, int B, int n_cta, float* o_part, float* ml_part,
+                                  const int32_t* seq_lens, int B, int n_q, int n_cta, float* o_part, float* ml_part,
                                   int32_t* meta, cudaStream_t s) {
   EncodeFn enc = get_encode();
   if (!enc) return cudaErrorNotSupported;
@@ -784,6 +795,7 @@ cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const 
   a.B = B; a.h_loc = g.h_loc; a.h_q = g.h_q; a.head_begin = g.head_begin; a.page_size = cache.page_size;
   a.max_pages = cache.max_pages_per_seq; a.scale_log2 = g.sm_scale * 1.4426950408889634f;
   a.cap = cache.max_pages_per_seq * cache.page_size;
+  a.n_q = n_q;
   a.trace = nullptr;
   a.trace_cta = 0;
   switch (g.w_lat) {

@@ -22,8 +22,9 @@ struct FArgs {
   const float* ml_part;     // [segs, H_loc, 2]
   const int32_t* meta;      // [B, 2] first / last segment of each sequence
   const uint16_t* W_UV;     // [H_loc, d_h, W_lat]
-  uint16_t* v;              // [B, H_loc * d_h]
+  uint16_t* v;              // [B * n_q, H_loc * d_h]
   int B, h_loc, w_lat, d_h;
+  int n_q;                  // query tokens per sequence: output row b' = b * n_q + i, partial row i * H_loc + h
 };
 
 __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
@@ -50,21 +51,23 @@ __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
   {
     const int m0 = blockIdx.y * kMB;
     // ---- combine: warp w merges rows b = m0 + w, m0 + w + 8, ...
+    const int n_rows = a.n_q * a.h_loc;             // partial rows per segment
     for (int bi = warp; bi < kMB; bi += kThreads / 32) {
-      const int b = m0 + bi;
+      const int bq = m0 + bi;                       // output row (sequence b, token i)
+      const int b = bq / a.n_q, prow = (bq % a.n_q) * a.h_loc + h;
       uint16_t* arow = sA + bi * WP;
-      if (b >= a.B) {
+      if (bq >= a.B * a.n_q) {
         for (int c = lane * 8; c < a.w_lat; c += 256) *reinterpret_cast<uint4*>(arow + c) = make_uint4(0, 0, 0, 0);
         continue;
       }
       const int s0 = a.meta[2 * b], s1 = a.meta[2 * b + 1];
       float M = -INFINITY;
-      for (int s = s0 + lane; s <= s1; s += 32) M = fmaxf(M, a.ml_part[((long)s * a.h_loc + h) * 2]);
+      for (int s = s0 + lane; s <= s1; s += 32) M = fmaxf(M, a.ml_part[((long)s * n_rows + prow) * 2]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
       float L = 0.f;
       for (int s = s0 + lane; s <= s1; s += 32) {
-        const float* ml = a.ml_part + ((long)s * a.h_loc + h) * 2;
+        const float* ml = a.ml_part + ((long)s * n_rows + prow) * 2;
         const float w = exp2f(ml[0] - M);
         if (s - s0 < 32) s_w[warp][s - s0] = w;         // first 32 segment weights, for the merge
         L += w * ml[1];
@@ -77,8 +80,8 @@ __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
 #pragma unroll 8
         for (int s = s0; s <= s1; ++s) {
           // (lanes past W_lat have left this loop: no warp-collective ops in here)
-          const float wgt = s - s0 < 32 ? s_w[warp][s - s0] : exp2f(a.ml_part[((long)s * a.h_loc + h) * 2] - M);
-          const float4* src = reinterpret_cast<const float4*>(a.o_part + ((long)s * a.h_loc + h) * a.w_lat + c);
+          const float wgt = s - s0 < 32 ? s_w[warp][s - s0] : exp2f(a.ml_part[((long)s * n_rows + prow) * 2] - M);
+          const float4* src = reinterpret_cast<const float4*>(a.o_part + ((long)s * n_rows + prow) * a.w_lat + c);
           const float4 x0 = src[0], x1 = src[1];
           acc[0] += wgt * x0.x; acc[1] += wgt * x0.y; acc[2] += wgt * x0.z; acc[3] += wgt * x0.w;
           acc[4] += wgt * x1.x; acc[5] += wgt * x1.y; acc[6] += wgt * x1.z; acc[7] += wgt * x1.w;
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
         for (int hh = 0; hh < 2; ++hh) {
           const int b = m0 + mw * 16 + (lane >> 2) + hh * 8;
           const int e = nw * 32 + ni * 8 + (lane & 3) * 2;
-          if (b < a.B)
+          if (b < a.B * a.n_q)
             *reinterpret_cast<uint32_t*>(a.v + (long)b * a.h_loc * a.d_h + h * a.d_h + e) =
                 pack_bf16(acc[ni][2 * hh], acc[ni][2 * hh + 1]);
         }
@@ -132,9 +135,9 @@ __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
 
 bool combine_wuv_supported(const Geom& g) { return g.d_h % 32 == 0 && g.w_lat % 64 == 0 && g.w_lat <= 512; }
 
-cudaError_t launch_combine_wuv(const Geom& g, int B, const float* o_part, const float* ml_part, const int32_t* meta,
-                               const uint16_t* W_UV, uint16_t* v, cudaStream_t s) {
-  FArgs a{o_part, ml_part, meta, W_UV, v, B, g.h_loc, g.w_lat, g.d_h};
+cudaError_t launch_combine_wuv(const Geom& g, int B, int n_q, const float* o_part, const float* ml_part,
+                               const int32_t* meta, const uint16_t* W_UV, uint16_t* v, cudaStream_t s) {
+  FArgs a{o_part, ml_part, meta, W_UV, v, B, g.h_loc, g.w_lat, g.d_h, n_q};
   const size_t smem = size_t(g.d_h + kMB) * (g.w_lat + 8) * 2;
   static bool attr = false;
   if (!attr) {
@@ -143,7 +146,7 @@ cudaError_t launch_combine_wuv(const Geom& g, int B, const float* o_part, const 
     attr = true;
   }
   KernelScope ks("K45_combine_W_UV", s);
-  return launch_k(combine_wuv_kernel, dim3(g.h_loc, (B + kMB - 1) / kMB), kThreads, smem, s, a);
+  return launch_k(combine_wuv_kernel, dim3(g.h_loc, (B * n_q + kMB - 1) / kMB), kThreads, smem, s, a);
 }
 
 }  // namespace tpla

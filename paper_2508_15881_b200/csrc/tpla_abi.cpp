@@ -201,8 +201,9 @@ SplitPlan choose_split(int B, int max_seq_len) {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-WsLayout ws_layout(const Geom& g, int B, int max_seq_len) {
+WsLayout ws_layout(const Geom& g, int B, int n_q, int max_seq_len) {
   WsLayout L{};
+  const int R = B * n_q;                                 // output rows (sequence, query token)
   SplitPlan sp = choose_split(B, max_seq_len);
   int K = g.h_loc * g.d_h;
   // split K = H_loc*d_h of the W^O GEMM into equal 64-multiples (at most 16) to fill the SMs
@@ -213,15 +214,16 @@ WsLayout ws_layout(const Geom& g, int B, int max_seq_len) {
   // for the persistent tcgen05 K3 (each CTA range touches at most one more sequence than it starts in)
   L.n_cta = tc_num_ctas(g, B, max_seq_len);
   const size_t parts = std::max(size_t(B) * sp.n_split, size_t(L.n_cta) + B);
+  const size_t rows = size_t(n_q) * g.h_loc;            // partial rows per segment / split
   size_t off = 0;
-  L.q_lat = off;   off += align256(size_t(B) * g.h_loc * g.w_lat * 2);
-  L.o_part = off;  off += align256(parts * g.h_loc * g.w_lat * 4);
-  L.ml_part = off; off += align256(parts * g.h_loc * 2 * 4);
-  L.o_lat = off;   off += align256(size_t(B) * g.h_loc * g.w_lat * 2);
-  L.v = off;       off += align256(size_t(B) * K * 2);
-  L.y_part = off;  off += align256(size_t(L.kslices) * B * g.D * 4);
+  L.q_lat = off;   off += align256(size_t(R) * g.h_loc * g.w_lat * 2);
+  L.o_part = off;  off += align256(parts * rows * g.w_lat * 4);
+  L.ml_part = off; off += align256(parts * rows * 2 * 4);
+  L.o_lat = off;   off += align256(size_t(R) * g.h_loc * g.w_lat * 2);
+  L.v = off;       off += align256(size_t(R) * K * 2);
+  L.y_part = off;  off += align256(size_t(L.kslices) * R * g.D * 4);
   L.meta = off;    off += align256(size_t(B) * 2 * 4);
-  L.wo_part = off; off += align256(wo_tc_supported(g.D, K, B) ? wo_tc_part_bytes(g.D, K, B) : 0);
+  L.wo_part = off; off += align256(wo_tc_supported(g.D, K, R) ? wo_tc_part_bytes(g.D, K, R) : 0);
   L.total = off;
   return L;
 }
@@ -240,7 +242,7 @@ static cudaError_t run_attention(const Geom& g, const tpla_cache& cache, const u
   cudaError_t e;
   if (use_tc_attention(g, B)) {
     auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
-    e = launch_decode_attn_tc(g, cache, q_lat, q_pe, seq_lens, B, L.n_cta, o_part, ml_part, meta, s);
+    e = launch_decode_attn_tc(g, cache, q_lat, q_pe, seq_lens, B, 1, L.n_cta, o_part, ml_part, meta, s);
     if (e != cudaSuccess || (!o_bf16 && !o_f32 && !lse)) return e;   // no output requested: K3 alone
     return launch_combine_seg(g, B, o_part, ml_part, meta, o_bf16, o_f32, lse, s);
   }
@@ -462,13 +464,18 @@ tpla_status tpla_prefill_mla(const tpla_config* cfg, const tpla_weights* w, cons
   return append_common(cfg, w, cache, c_kv, k_pe, seq_idx, pos, n, TPLA_RMS_EXACT, nullptr, stream);
 }
 
-tpla_status tpla_decode_workspace_bytes(const tpla_config* cfg, int32_t B, int32_t max_seq_len, size_t* bytes) {
+tpla_status tpla_decode_workspace_bytes_mtp(const tpla_config* cfg, int32_t B, int32_t n_q, int32_t max_seq_len,
+                                            size_t* bytes) {
   Geom g{};
   tpla_status st = make_geom(cfg, &g);
   if (st) return st;
-  if (B < 1 || max_seq_len < 1 || !bytes) return fail(TPLA_ERR_INVALID_ARG, "bad B/max_seq_len");
-  *bytes = ws_layout(g, B, max_seq_len).total;
+  if (B < 1 || n_q < 1 || max_seq_len < 1 || !bytes) return fail(TPLA_ERR_INVALID_ARG, "bad B/n_q/max_seq_len");
+  *bytes = ws_layout(g, B, n_q, max_seq_len).total;
   return ok();
+}
+
+tpla_status tpla_decode_workspace_bytes(const tpla_config* cfg, int32_t B, int32_t max_seq_len, size_t* bytes) {
+  return tpla_decode_workspace_bytes_mtp(cfg, B, 1, max_seq_len, bytes);
 }
 
 static tpla_status check_decode_common(const Geom& g, const tpla_cache* cache, const void* q_pe,
@@ -488,10 +495,23 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
                         const void* q_nope, const void* q_pe, const int32_t* seq_lens, int32_t B,
                         int32_t max_seq_len, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,
                         tpla_comm* comm, void* stream) {
+  return tpla_decode_mtp(cfg, w, cache, q_nope, q_pe, seq_lens, B, 1, max_seq_len, ws, ws_bytes, y, out, flags, comm,
+                         stream);
+}
+
+tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                            const void* q_nope, const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t n_q,
+                            int32_t max_seq_len, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,
+                            tpla_comm* comm, void* stream) {
   Geom g{};
   tpla_status st = make_geom(cfg, &g);
   if (st) return st;
   if ((st = check_decode_common(g, cache, q_pe, seq_lens, B, max_seq_len))) return st;
+  if (n_q < 1) return fail(TPLA_ERR_INVALID_ARG, "n_q=%d", n_q);
+  if (n_q > 1 && !(use_tc_attention(g, B) && combine_wuv_supported(g) && n_q * g.h_loc <= 128))
+    return fail(TPLA_ERR_UNSUPPORTED, "multi-token decode needs the tcgen05 path and n_q*H_loc <= 128 (n_q=%d, H_loc=%d)",
+                n_q, g.h_loc);
+  const int R = B * n_q;                                  // output rows (sequence, token)
   if (!w || !w->W_UK || !w->W_UV || !w->W_O) return fail(TPLA_ERR_INVALID_ARG, "NULL weights");
   if (!q_nope || !y || !ws) return fail(TPLA_ERR_INVALID_ARG, "NULL q_nope/y/ws");
   if (!aligned16(q_nope) || !aligned16(ws) || !aligned16(y)) return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
@@ -500,7 +520,7 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
   // so the communicator spans k/m processes for some m >= 1.
   if (comm && (g.k % comm->world))
     return fail(TPLA_ERR_INVALID_ARG, "communicator world %d does not divide k=%d", comm->world, g.k);
-  WsLayout L = ws_layout(g, B, max_seq_len);
+  WsLayout L = ws_layout(g, B, n_q, max_seq_len);
   if (ws_bytes < L.total) return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(ws);
@@ -512,7 +532,7 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
   cudaError_t e;
   // K2: Q'_j[b,h,:] = W^UK'_j[h] q[b,h,:]   (mu_j folded)
   e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK), qn + size_t(g.head_begin) * g.d_h,
-                       long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h, B, q_lat, true, s);
+                       long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h, R, q_lat, true, s);
   if (e != cudaSuccess) return cuda_fail(e, "K2 absorb_q");
   if (use_tc_attention(g, B) && combine_wuv_supported(g)) {
     // K3: per-shard split-K flash decoding (Eq. tpla_softmax_one_device) -> partials;
@@ -520,10 +540,10 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
     auto* o_part = reinterpret_cast<float*>(base + L.o_part);
     auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
     auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
-    e = launch_decode_attn_tc(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, L.n_cta, o_part,
-                              ml_part, meta, s);
+    e = launch_decode_attn_tc(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, n_q, L.n_cta,
+                              o_part, ml_part, meta, s);
     if (e != cudaSuccess) return cuda_fail(e, "K3 decode attention");
-    e = launch_combine_wuv(g, B, o_part, ml_part, meta, static_cast<const uint16_t*>(w->W_UV), v, s);
+    e = launch_combine_wuv(g, B, n_q, o_part, ml_part, meta, static_cast<const uint16_t*>(w->W_UV), v, s);
     if (e != cudaSuccess) return cuda_fail(e, "K4+K5a combine/W_UV");
   } else {
     // K3 + K4: per-shard split-K flash decoding (Eq. tpla_softmax_one_device) -> O_j
@@ -540,25 +560,25 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
   const int Kw = g.h_loc * g.d_h;
   const char* force = getenv("TPLA_WO");
   bool out_done = false;
-  if (wo_tc_supported(g.D, Kw, B) && !(force && strcmp(force, "mma") == 0)) {
+  if (wo_tc_supported(g.D, Kw, R) && !(force && strcmp(force, "mma") == 0)) {
     // without an all-reduce the segment reduce also writes the bf16 output (no cast launch)
     uint16_t* out16 = comm ? nullptr : static_cast<uint16_t*>(out);
-    e = launch_wo_tc(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, B, base + L.wo_part, y, accumulate, out16, s);
+    e = launch_wo_tc(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, R, base + L.wo_part, y, accumulate, out16, s);
     if (e != cudaSuccess) return cuda_fail(e, "K5b W_O (tcgen05)");
     out_done = out16 != nullptr;
   } else {
-    e = launch_skinny_gemm(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, B, L.kslices, y_part, s);
+    e = launch_skinny_gemm(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, R, L.kslices, y_part, s);
     if (e != cudaSuccess) return cuda_fail(e, "K5b W_O");
-    e = launch_reduce_slices(y_part, L.kslices, B, g.D, y, accumulate, s);
+    e = launch_reduce_slices(y_part, L.kslices, R, g.D, y, accumulate, s);
     if (e != cudaSuccess) return cuda_fail(e, "K5b reduce");
   }
   // C1: O = AllReduce(Σ_r Õ_r)
   if (comm) {
-    ncclResult_t r = g_nccl.AllReduce(y, y, size_t(B) * g.D, ncclFloat32, ncclSum, comm->comm, s);
+    ncclResult_t r = g_nccl.AllReduce(y, y, size_t(R) * g.D, ncclFloat32, ncclSum, comm->comm, s);
     if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
   }
   if (out && !out_done) {
-    e = launch_cast_bf16(y, long(B) * g.D, static_cast<uint16_t*>(out), s);
+    e = launch_cast_bf16(y, long(R) * g.D, static_cast<uint16_t*>(out), s);
     if (e != cudaSuccess) return cuda_fail(e, "cast");
   }
   return ok();
@@ -574,7 +594,7 @@ tpla_status tpla_decode_attention(const tpla_config* cfg, const tpla_cache* cach
   if (!q_lat || !ws) return fail(TPLA_ERR_INVALID_ARG, "NULL q_lat/ws");
   if (!O && lse) return fail(TPLA_ERR_INVALID_ARG, "lse requires O");
   if (!aligned16(q_lat) || !aligned16(ws)) return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
-  WsLayout L = ws_layout(g, B, max_seq_len);
+  WsLayout L = ws_layout(g, B, 1, max_seq_len);
   if (ws_bytes < L.total) return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(ws);

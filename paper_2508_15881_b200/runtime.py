@@ -53,7 +53,8 @@ class TplaRank:
     """One device's share of a TPLA layer (plan, weights, cache, workspace)."""
 
     def __init__(self, spec: LayerSpec, *, k: int, g: int, rank: int, batch: int, max_seq_len: int,
-                 page_size: int = 64, device="cuda", page_perm_seed: int | None = None, extra_pages: int = 0):
+                 page_size: int = 64, device="cuda", page_perm_seed: int | None = None, extra_pages: int = 0,
+                 n_q: int = 1):
         self.spec = spec
         self.k, self.g, self.rank = k, g, rank
         self.cfg = make_config(spec, k, g, rank)
@@ -73,7 +74,8 @@ class TplaRank:
         self.block_table = torch.from_numpy(self.block_table_host).to(self.device)
         self.cache = abi.tpla_cache(self.cache_buf.data_ptr(), self.block_table.data_ptr(), num_pages, page_size,
                                     self.max_pages, self.row_stride, batch)
-        self.ws_bytes = abi.tpla_decode_workspace_bytes(self.cfg, batch, max_seq_len)
+        self.n_q = n_q                  # query tokens per sequence the workspace is sized for (decode_mtp)
+        self.ws_bytes = abi.tpla_decode_workspace_bytes_mtp(self.cfg, batch, n_q, max_seq_len)
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.weights = None
         self._wbufs = None
@@ -115,6 +117,13 @@ class TplaRank:
         B = int(q_nope.shape[0]) if B is None else B
         abi.tpla_decode(self.cfg, self.weights, self.cache, q_nope, q_pe, seq_lens, B, self.max_seq_len, self.ws,
                         self.ws_bytes, y, out, abi.DECODE_ACCUMULATE if accumulate else 0, comm, stream_ptr(stream))
+
+    def decode_mtp(self, q_nope, q_pe, seq_lens, y, out=None, *, accumulate=False, comm=None, stream=None):
+        """Multi-token decode: q_nope [B, n_q, h_q, d_h], q_pe [B, n_q, h_q, d_r]; y/out [B * n_q, D]."""
+        B, n_q = int(q_nope.shape[0]), int(q_nope.shape[1])
+        abi.tpla_decode_mtp(self.cfg, self.weights, self.cache, q_nope, q_pe, seq_lens, B, n_q, self.max_seq_len,
+                            self.ws, self.ws_bytes, y, out, abi.DECODE_ACCUMULATE if accumulate else 0, comm,
+                            stream_ptr(stream))
 
     def decode_attention(self, q_lat, q_pe, seq_lens, O, lse=None, *, B: int | None = None, stream=None):
         B = int(q_lat.shape[0]) if B is None else B

@@ -303,6 +303,77 @@ def test_e2e_parity_kimi_shape():
     e2e_case(dev(), synth.PRESETS["kimi"], 4, 4, "hadamard", [64, 129])
 
 
+def mtp_case(d, dims, k, g, n_q, S_list, *, seed=0, kind="hadamard"):
+    """Multi-token decode: the n_q newest tokens of each sequence are decoded in one
+    step.  Pinned against the oracle's single-token step over each token's causal prefix: token i
+    of sequence b sees the first S_b - n_q + 1 + i rows (P:137-141 per token)."""
+    B = len(S_list)
+    xf, sseed, U, U32, alpha = transform_inputs(kind, dims, 31, g)
+    basis = U if kind == "pca" else None
+    w = synth.gen_weights(dims, seed + 1)
+    qb, qpeb = synth.gen_queries(dims, B * n_q, seed + 2)
+    qb = qb.reshape(B, n_q, dims.h_q, dims.d_h)
+    qpeb = qpeb.reshape(B, n_q, dims.h_q, dims.d_r)
+    c_raw = [synth.gen_raw_ckv(dims, S, seed + 3, b, basis=basis) for b, S in enumerate(S_list)]
+    k_pe = [synth.gen_kpe(dims, S, seed + 3, b) for b, S in enumerate(S_list)]
+    n_prompt = [S - n_q for S in S_list]
+    y = torch.zeros((B * n_q, dims.D), dtype=torch.float32, device=d)
+    out = torch.empty((B * n_q, dims.D), dtype=torch.bfloat16, device=d)
+    lens = torch.tensor(S_list, dtype=torch.int32, device=d)
+    for rid in range(k):
+        r = TplaRank(spec_of(dims), k=k, g=g, rank=rid, batch=B, max_seq_len=max(S_list), device=d, n_q=n_q,
+                     page_perm_seed=rid + 3)
+        r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=xf, sign_seed=sseed, U_pca=U32, alpha=alpha)
+        # prompt rows EXACT (prefill), the n_q new rows SLICED (appended by the decode step's K1)
+        seq = np.concatenate([np.full(n, b, np.int32) for b, n in enumerate(n_prompt)])
+        pos = np.concatenate([np.arange(n, dtype=np.int32) for n in n_prompt])
+        r.prefill(bf16_from_bits(np.concatenate([c[:n] for c, n in zip(c_raw, n_prompt)]), d),
+                  bf16_from_bits(np.concatenate([x[:n] for x, n in zip(k_pe, n_prompt)]), d),
+                  torch.from_numpy(seq).to(d), torch.from_numpy(pos).to(d))
+        seq = np.repeat(np.arange(B, dtype=np.int32), n_q)
+        pos = np.concatenate([np.arange(n, n + n_q, dtype=np.int32) for n in n_prompt])
+        r.append(bf16_from_bits(np.concatenate([c[n:] for c, n in zip(c_raw, n_prompt)]), d),
+                 bf16_from_bits(np.concatenate([x[n:] for x, n in zip(k_pe, n_prompt)]), d),
+                 torch.from_numpy(seq).to(d), torch.from_numpy(pos).to(d), abi.RMS_SLICED)
+        r.decode_mtp(bf16_from_bits(qb, d), bf16_from_bits(qpeb, d), lens, y, out if rid == k - 1 else None,
+                     accumulate=rid > 0)
+    torch.cuda.synchronize()
+    got = y.cpu().numpy().reshape(B, n_q, dims.D)
+    for i in range(n_q):
+        lim = [S - n_q + 1 + i for S in S_list]
+        pb = tpla.Problem(W_UK=f64(w.W_UK), W_UV=f64(w.W_UV), gamma=f64(w.gamma), W_O=f64(w.W_O), U=U,
+                          alpha=np.asarray(alpha, float), mu=np.asarray(alpha, float),
+                          c_raw=[f64(c[:L]) for c, L in zip(c_raw, lim)], k_pe=[f64(x[:L]) for x, L in zip(k_pe, lim)],
+                          modes=[[tpla.EXACT] * n + [tpla.SLICED] * (L - n) for n, L in zip(n_prompt, lim)],
+                          q_nope=f64(qb[:, i]), q_pe=f64(qpeb[:, i]), h_q=dims.h_q, d_h=dims.d_h, eps=1e-6,
+                          sm_scale=dims_scale(dims))
+        ref = tpla.tpla_decode_step(pb, k, g, round_rows=numerics.round_bf16)
+        e = row_rel_err(got[:, i], ref)
+        assert e <= TOL, (i, e)
+    assert torch.equal(out, y.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("dname,k,g,n_q", [("kimi", 4, 4, 2), ("dsv3", 4, 2, 2), ("dsv3", 8, 2, 4), ("kimi", 8, 4, 4),
+                                           ("dsv3", 2, 1, 2)])
+def test_multi_token_decode(dname, k, g, n_q):
+    # lengths around tile edges: a segment may hold no visible token for the earlier rows
+    mtp_case(dev(), synth.PRESETS[dname], k, g, n_q, [n_q, 65, 129, 300])
+
+
+def test_multi_token_decode_rejects_too_many_rows():
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    r = TplaRank(spec_of(dims), k=2, g=2, rank=0, batch=1, max_seq_len=64, device=d, n_q=2)
+    w = synth.gen_weights(dims, 1)
+    r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_HADAMARD)
+    q = torch.zeros((1, 2, dims.h_q, dims.d_h), dtype=torch.bfloat16, device=d)
+    qpe = torch.zeros((1, 2, dims.h_q, dims.d_r), dtype=torch.bfloat16, device=d)
+    y = torch.zeros((2, dims.D), dtype=torch.float32, device=d)
+    with pytest.raises(abi.TplaError) as ei:            # 2 tokens x 128 heads > 128 MMA rows
+        r.decode_mtp(q, qpe, torch.tensor([64], dtype=torch.int32, device=d), y)
+    assert ei.value.status == abi.ERR_UNSUPPORTED
+
+
 def test_deterministic_graph_replay_and_fused_bf16_out():
     """DSV3 shape, k = g = 2 on this GPU: the decode is bitwise deterministic, a CUDA-graph capture
     of it (PDL launches inside) replays to the same bits, and the bf16 output written by the W^O
