@@ -95,6 +95,11 @@ struct Cfg {
   // once; at W_lat <= 128 the MMA work per 64-token tile is too short to hide those (measured),
   // so the larger tile halves the synchronisation per byte.
   static constexpr int TT = WL <= 128 ? 128 : 64;
+  // S (= P) buffers in TMEM.  Three when they fit (W_lat = 64: O 64 + Q' 32 + 3 x 128 = 480
+  // columns): QK then runs two tiles ahead of PV, so S(g+1) is ready when the softmax finishes
+  // tile g (with two buffers the softmax waited ~470 cycles per tile for it, measured).
+  static constexpr int NSB = W_LAT == 64 ? 3 : 2;
+  static constexpr int LAG = NSB - 1;                 // PV issued LAG tiles behind QK
   static constexpr int SUB = TT / kSub;               // TMA boxes per column group per tile
   static constexpr int CH = TT / 2;                   // S columns per softmax warp
   static constexpr int SEQ_COST = 512 / TT;           // per-sequence header cost in tiles (schedule)
@@ -111,7 +116,7 @@ struct Cfg {
   static constexpr int O_COL = 0;
   static constexpr int Q_COL = WL;                    // WL/2 columns of packed bf16
   static constexpr int S_COL0 = (WL + WL / 2 + 63) / 64 * 64;
-  static constexpr int S_COLS = S_COL0 + 2 * TT;
+  static constexpr int S_COLS = S_COL0 + NSB * TT;
   static constexpr int TMEM_COLS = S_COLS <= 256 ? 256 : 512;
   static_assert(S_COLS <= 512, "TMEM budget");
 };
@@ -166,13 +171,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
                                                                    // then the send staging buffer (same shape)
   uint8_t* s_kv = smem + C::QPE_BYTES + C::XCH_BYTES;
   __shared__ uint64_t kv_full[C::NST], kv_empty[C::NST];
-  __shared__ uint64_t s_full[2], p_full[2], pv_done[2], q_ready;
+  __shared__ uint64_t s_full[C::NSB], p_full[C::NSB], pv_done[C::NSB], q_ready;
   __shared__ uint32_t tmem_base;
   __shared__ int cum[kMaxB + 1];
   __shared__ int slen[kMaxB];            // min(seq_len, capacity) per sequence
   __shared__ int lo_arr[kMaxCta + 1];    // first tile of every CTA's range (+ the end)
   __shared__ int s_before;
-  __shared__ float red_max[2][2][128];   // [tile parity][half][row] partial row maxima
+  __shared__ float red_max[C::NSB][2][128];   // [S buffer][half][row] partial row maxima
   __shared__ float red_l[2][128];        // [half][row] partial row sums at a segment end
   __shared__ uint64_t x_full[8], x_ok[8]; // PAIR, per softmax warp: peer's logits landed / peer read ours
 
@@ -185,7 +190,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap);
     for (int i = 0; i < C::NST; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 8); mbar_init(&pv_done[i], 1); }
+    for (int i = 0; i < C::NSB; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 8); mbar_init(&pv_done[i], 1); }
     mbar_init(&q_ready, 8);      // p_full / q_ready: one arrival per softmax warp (elected lane)
     if (C::PAIR)
       for (int i = 0; i < 8; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_ok[i], 1); }
@@ -319,25 +324,26 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     int g = 0, seg = 0;
     auto issue_pv = [&](int gp, bool first_pv) {
       const int st = gp % C::NST;
-      mbar_wait(&p_full[gp & 1], (gp >> 1) & 1);
+      mbar_wait(&p_full[gp % C::NSB], (gp / C::NSB) & 1);
       tc_fence_after();
       if (elect_one()) {
         TRACE(1, gp);
         // V = latent boxes of the tile, MN-major: 64-column atoms one box (8 KB) apart
         const uint64_t v_desc = make_desc(kv0 + st * C::STAGE_BYTES, C::BOX_BYTES, hi_k);
-        const uint32_t p_tmem = tb + C::S_COL0 + (gp & 1) * C::TT;
+        const uint32_t p_tmem = tb + C::S_COL0 + (gp % C::NSB) * C::TT;
 #pragma unroll
         for (int kk = 0; kk < C::TT / 16; ++kk)      // 16 tokens (2 KB of rows) per step
           mma_ts(tb + C::O_COL, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), id_pv,
                  (first_pv && kk == 0) ? 0u : 1u);
         mma_commit(&kv_empty[st]);
-        mma_commit(&pv_done[gp & 1]);
+        mma_commit(&pv_done[gp % C::NSB]);
         TRACE(5, gp);
       }
       __syncwarp();
     };
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
+      const int g0 = g;
       mbar_wait(&q_ready, seg & 1);
       tc_fence_after();
       for (int t = t0; t < t1; ++t, ++g) {
@@ -347,7 +353,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         if (elect_one()) {
           TRACE(0, g);
           const uint64_t kv_desc = make_desc(kv0 + st * C::STAGE_BYTES, 16, hi_k);
-          const uint32_t s_tmem = tb + C::S_COL0 + (g & 1) * C::TT;
+          const uint32_t s_tmem = tb + C::S_COL0 + (g % C::NSB) * C::TT;
 #pragma unroll
           for (int kk = 0; kk < C::WL / 16; ++kk)     // Q'_j (TMEM) x ĉ tileᵀ: box kk/4, +32 B per k-step
             mma_ts(s_tmem, tb + C::Q_COL + kk * 8,
@@ -358,13 +364,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           for (int kk = (C::PAIR ? 2 * int(crank) : 0); kk < (C::PAIR ? 2 * int(crank) + 2 : 4); ++kk)
             mma_ss(s_tmem, qpe_desc + uint64_t(kk * 2),
                    kv_desc + uint64_t(((C::NBOX - 1) * C::BOX_BYTES + kk * 32) >> 4), id_qk, 1u);
-          mma_commit(&s_full[g & 1]);
+          mma_commit(&s_full[g % C::NSB]);
           TRACE(4, g);
         }
         __syncwarp();
-        if (t > t0) issue_pv(g - 1, t - 1 == t0);
+        if (t - t0 >= C::LAG) issue_pv(g - C::LAG, g - C::LAG == g0);
       }
-      issue_pv(g - 1, t1 - 1 == t0);
+      for (int gp = max(g0, g - C::LAG); gp < g; ++gp) issue_pv(gp, gp == g0);
     }
   } else if (warp >= 4) {
     // ============================================================ softmax / Q loader / epilogue
@@ -427,9 +433,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       float m_used = -INFINITY;                          // running max, log2 units (same in both halves)
       float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;      // this half's running sum (4 chains)
       for (int t = t0; t < t1; ++t, ++g) {
-        const int sb = g & 1;
+        const int sb = g % C::NSB;
         if (warp == 4 && lane == 0) TRACE(18, g);
-        mbar_wait(&s_full[sb], (g >> 1) & 1);
+        mbar_wait(&s_full[sb], (g / C::NSB) & 1);
         if (warp == 4 && lane == 0) TRACE(2, g);
         if (!q_active) {                                 // no head rows here: P stays 0 (S rows are 0)
           if (lane == 0) mbar_arrive(&p_full[sb]);
@@ -516,7 +522,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           if (t > t0) {
             // O holds PV(g-1) and earlier: wait for it, then scale this half's O columns
             const float f = need ? ex2(m_used - m_new) : 1.f;
-            mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+            mbar_wait(&pv_done[(g - 1) % C::NSB], ((g - 1) / C::NSB) & 1);
             tc_fence_after();
 #pragma unroll 1
             for (int c0 = half * (C::WL / 2); c0 < (half + 1) * (C::WL / 2); c0 += 32) {
@@ -582,7 +588,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       // ---- epilogue of the segment: unnormalised partial (O, m, l)
       float l = (l0 + l1) + (l2 + l3);
       red_l[half][r] = l;
-      mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+      mbar_wait(&pv_done[(g - 1) % C::NSB], ((g - 1) / C::NSB) & 1);
       tc_fence_after();
       named_bar_sync(pair_bar, 64);
       l += red_l[half ^ 1][r];
