@@ -2,6 +2,7 @@
 // 148 CTAs x W warps, 8 independent chains per thread.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 tools/mufu_rate.cu -o tools/mufu_rate
 #include <cuda_runtime.h>
+#include <stdint.h>
 #include <stdio.h>
 
 constexpr int kIters = 4096;
@@ -18,8 +19,14 @@ __global__ void rate_kernel(float* out, long long* cyc) {
     for (int i = 0; i < 8; ++i) {
       if (OP == 0) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[i]));
       else if (OP == 1) asm volatile("fma.rn.f32 %0, %0, 0.999, -0.001;" : "+f"(v[i]));
-      else { // FA4-style mix: 1 ex2 + 3 ffma
-        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[i]));
+      else if (OP == 2) {   // ex2.approx.f16x2: two exponentials per instruction
+        uint32_t u = __float_as_uint(v[i]);
+        asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(u));
+        v[i] = __uint_as_float(u);
+      } else {              // ex2.approx.ftz.bf16x2
+        uint32_t u = __float_as_uint(v[i]);
+        asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(u));
+        v[i] = __uint_as_float(u);
       }
     }
   }
@@ -55,6 +62,8 @@ void run(const char* name, int threads) {
 int main() {
   for (int t : {128, 256, 512, 1024}) run<0>("ex2", t);
   for (int t : {128, 256, 1024}) run<1>("ffma", t);
+  for (int t : {256, 1024}) run<2>("ex2.f16x2 (instr)", t);
+  for (int t : {256, 1024}) run<3>("ex2.bf16x2 (instr)", t);
   printf("MUFU OK\n");
   return 0;
 }
