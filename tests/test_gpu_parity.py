@@ -294,7 +294,7 @@ def test_e2e_parity_tiny(dname, k, g, kind):
 
 
 @pytest.mark.parametrize("k,g,kind", [(2, 2, "hadamard"), (2, 2, "pca"), (4, 4, "hadamard"), (8, 8, "hadamard"),
-                                      (4, 2, "identity"), (1, 1, "identity"), (2, 1, "hadamard")])
+                                      (4, 2, "identity"), (8, 2, "hadamard"), (1, 1, "identity"), (2, 1, "hadamard")])
 def test_e2e_parity_dsv3_shape(k, g, kind):
     e2e_case(dev(), synth.PRESETS["dsv3"], k, g, kind, [5, 200, 333])
 
