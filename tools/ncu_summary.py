@@ -23,6 +23,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("csv")
     ap.add_argument("--decode-grid", type=int, default=8, help="append launches with grid.x <= this are decode K1")
+    ap.add_argument("--cap", type=int, default=0,
+                    help="count at most this many launches per kernel (the first ones): drops launches outside "
+                         "the decode steps, e.g. bench.py's K3-alone graph")
     a = ap.parse_args()
     rows = [r for r in csv.reader(open(a.csv)) if len(r) > 14 and r[0] != "ID" and "tpla::" in r[4]]
     per = collections.defaultdict(list)
@@ -32,6 +35,8 @@ def main():
         gx = int(r[8].strip("()").split(",")[0])
         if name.startswith("append_kernel") and gx > a.decode_grid:
             continue                          # prefill cache fill, not part of the decode step
+        if a.cap and len(per[name]) >= a.cap:
+            continue
         per[name].append(float(r[14]) / 1e3)  # ns -> us
         grids[name] = (r[8], r[7])
     tot = sum(sum(v) for v in per.values())
