@@ -775,10 +775,15 @@ bool tc_attention_supported(const Geom& g, int B) {
          B <= kMaxB;
 }
 
+// At least kMinBoxes 64-token boxes per CTA: with one box each (small batch x short context) a
+// CTA's fixed costs dominate — its epilogue writes a 128 x W_lat fp32 partial (3x the bytes of a
+// 64-token C1 tile) and the merge then reads one partial per CTA (measured at batch 1, 4K: K3
+// 19 us and K45 26 us per rank with 64 one-box CTAs).
+constexpr long kMinBoxes = 4;
 int tc_num_ctas(const Geom& g, int B, int max_seq_len) {
-  long tiles = (long)B * ((max_seq_len + kSub - 1) / kSub);
+  long boxes = (long)B * ((max_seq_len + kSub - 1) / kSub);
   const int slots = g.w_lat == 512 ? num_sms() / 2 : num_sms();   // W_lat = 512: CTA pairs
-  return int(std::max(1L, std::min<long>(std::min(slots, kMaxCta), tiles)));
+  return int(std::max(1L, std::min<long>(std::min(slots, kMaxCta), boxes / kMinBoxes)));
 }
 
 cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
