@@ -74,6 +74,10 @@ def parse():
     p.add_argument("--batch", type=int, default=None, help="override the workload batch (sweep)")
     p.add_argument("--seq-len", type=int, default=None, help="override the workload context length (sweep)")
     p.add_argument("--no-graph", action="store_true", help="issue the timed steps eagerly instead of a CUDA graph")
+    p.add_argument("--wo", default="auto", choices=["auto", "rank", "shared"],
+                   help="up-projection: 'rank' = every rank multiplies its own v_j by its W^O rows (P:139-141); "
+                        "'shared' = the g ranks of a head block sum v first and read W^O once, reduce-scattered "
+                        "across processes (SURVEY f2(ii)); auto = shared when g > 1")
     p.add_argument("--profile-region", action="store_true",
                    help="cudaProfilerStart/Stop around the timed region (for ncu --profile-from-start off)")
     return p.parse_args()
@@ -284,7 +288,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2508_15881_b200 import abi
-    from paper_2508_15881_b200.runtime import LayerSpec, TplaRank, bf16_from_bits
+    from paper_2508_15881_b200.runtime import LayerSpec, TplaRank, bf16_from_bits, group_process_sets, head_block_groups
 
     wl = dict(WORKLOADS[args.workload])
     if args.batch:
@@ -348,6 +352,18 @@ def main():
         obj = [abi.tpla_comm_unique_id() if proc == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         comm = abi.tpla_comm_init(obj[0], N, proc)
+    wo = args.wo if args.wo != "auto" else ("shared" if g > 1 else "rank")
+    groups = head_block_groups(k, g, N, proc) if wo == "shared" else []
+    gcomms = {}
+    if wo == "shared":
+        for ps in group_process_sets(k, g, N):               # one communicator per process set, global order
+            obj = [abi.tpla_comm_unique_id() if proc == ps[0] else None]
+            dist.broadcast_object_list(obj, src=ps[0])
+            if proc in ps:
+                gcomms[ps] = abi.tpla_comm_init(obj[0], len(ps), ps.index(proc))
+    by_id = {rk.rank: rk for rk in ranks}
+    v_acc = [torch.zeros(by_id[grp.local_ranks[0]].v_acc_shape(B * nq, grp.n_chunks), dtype=torch.float32, device=dev)
+             for grp in groups]
     stream = torch.cuda.current_stream()
 
     def step(i, ck=None, kp=None, q=None, qq=None, o=None):
@@ -358,6 +374,16 @@ def main():
         o = out if o is None else o
         for rk in ranks:
             rk.append(ck, kp, seq_idx, pos_new, abi.RMS_SLICED)
+        if wo == "shared":
+            for grp, va in zip(groups, v_acc):
+                for j, r in enumerate(grp.local_ranks):
+                    by_id[r].decode_v(q, qq, seq_lens, va, n_chunks=grp.n_chunks, accumulate=j > 0)
+            for gi, (grp, va) in enumerate(zip(groups, v_acc)):
+                last = gi == len(groups) - 1
+                by_id[grp.local_ranks[0]].project_out(va, y, o if last else None, chunk=grp.chunk, accumulate=gi > 0,
+                                                      group_comm=gcomms.get(grp.procs),
+                                                      comm=comm if last else None)
+            return
         for j, rk in enumerate(ranks):
             last = j == len(ranks) - 1
             if nq == 1:
@@ -567,11 +593,17 @@ def main():
 
     if comm is not None:
         abi.tpla_comm_destroy(comm)
+    for c in gcomms.values():
+        abi.tpla_comm_destroy(c)
     if proc == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "us_per_layer": ms_step * 1e3,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic", "impl": "tpla", "config": config_of(wl, N, k, g),
+                "up_projection": ("shared: the latent group's v_j summed first (co-located ranks in place; across "
+                                  "GPUs a reduce-scatter over column chunks), W^O read once per head block "
+                                  "(SURVEY f2(ii); Σ_j v_j W^O_i = (Σ_j v_j) W^O_i, P:363)" if wo == "shared" else
+                                  "rank: every rank multiplies its own v_j by its W^O rows (P:139-141)"),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "gpu_launches_per_step": launches / args.steps, "clocks": clocks.summary(), "kernels": kernels,
                 "cuda_graph": graph is not None,

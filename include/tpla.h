@@ -211,6 +211,28 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
  *   ws: tpla_decode_workspace_bytes_mtp(cfg, B, n_q, max_seq_len) bytes.  tpla_decode = n_q 1. */
 tpla_status tpla_decode_workspace_bytes_mtp(const tpla_config* cfg, int32_t B, int32_t n_q, int32_t max_seq_len,
                                             size_t* bytes);
+
+/* Up-projection shared by a latent group.  The g devices j of head block i hold
+ * the same W^O rows, so Õ_i = Σ_j v_j W^O_i = (Σ_j v_j) W^O_i: the group may sum its
+ * v_j = O_j W^UV'_j first and read W^O once instead of g times.  Co-located devices add into one v_acc;
+ * devices in different processes reduce-scatter it over its column chunks and each projects its
+ * chunk's K-slice of W^O (1/n_chunks of the rows), then the usual all-reduce of y.
+ * v_acc layout: fp32, column-chunk-major [n_chunks][B * n_q][K / n_chunks], K = H_loc * d_h, i.e.
+ * element (row, col) at ((col / kc) * B*n_q + row) * kc + col % kc, kc = K / n_chunks (64 * n_chunks | K).
+ *   tpla_decode_v:    K2, K3, K4+K5a of this device into v_acc (= v_j, or += with TPLA_DECODE_ACCUMULATE).
+ *                     Needs the tcgen05 attention path; same inputs and workspace as tpla_decode_mtp.
+ *   tpla_project_out: with group_comm (world n_chunks, rank chunk): in-place ncclReduceScatter of v_acc
+ *                     (sum over the group; chunk `chunk` lands in place), then for every caller
+ *                     y [R, D] fp32 (=, or += with TPLA_DECODE_ACCUMULATE) = bf16(v_acc chunk) ·
+ *                     W^O[chunk's K rows]; then the all-reduce of y over comm (if given) and the bf16
+ *                     out [R, D] (or NULL).  Without group_comm the chunk must already hold the group
+ *                     sum.  ws: a decode workspace for at least R = B * n_q rows.  Errors as tpla_decode. */
+tpla_status tpla_decode_v(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache, const void* q_nope,
+                          const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t n_q, int32_t max_seq_len,
+                          void* ws, size_t ws_bytes, float* v_acc, int32_t n_chunks, int32_t flags, void* stream);
+tpla_status tpla_project_out(const tpla_config* cfg, const tpla_weights* w, float* v_acc, int32_t R, int32_t n_chunks,
+                             int32_t chunk, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,
+                             tpla_comm* group_comm, tpla_comm* comm, void* stream);
 tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
                             const void* q_nope, const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t n_q,
                             int32_t max_seq_len, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,

@@ -80,6 +80,10 @@ _SIGS = {
     "tpla_decode": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _P, _I, _I, _P,
                      _S, _P, _P, _I, _P, _P], _I),
     "tpla_decode_workspace_bytes_mtp": ([C.POINTER(tpla_config), _I, _I, _I, C.POINTER(_S)], _I),
+    "tpla_decode_v": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _P, _I, _I, _I,
+                       _P, _S, _P, _I, _I, _P], _I),
+    "tpla_project_out": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), _P, _I, _I, _I, _P, _S, _P, _P, _I, _P,
+                          _P, _P], _I),
     "tpla_decode_mtp": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _P, _I, _I,
                          _I, _P, _S, _P, _P, _I, _P, _P], _I),
     "tpla_decode_attention": ([C.POINTER(tpla_config), C.POINTER(tpla_cache), _P, _P, _P, _I, _I, _P, _S, _P, _P,
@@ -208,6 +212,19 @@ def tpla_decode_mtp(cfg, w, cache, q_nope, q_pe, seq_lens, B, n_q, max_seq_len, 
     _check(_lib.tpla_decode_mtp(C.byref(cfg), C.byref(w), C.byref(cache), _ptr(q_nope), _ptr(q_pe), _ptr(seq_lens), B,
                                 n_q, max_seq_len, _ptr(ws), ws_bytes, _ptr(y), _ptr(out), flags, comm, _ptr(stream)),
            "tpla_decode_mtp")
+
+
+def tpla_decode_v(cfg, w, cache, q_nope, q_pe, seq_lens, B, n_q, max_seq_len, ws, ws_bytes, v_acc, n_chunks=1, flags=0,
+                  stream=0):
+    _check(_lib.tpla_decode_v(C.byref(cfg), C.byref(w), C.byref(cache), _ptr(q_nope), _ptr(q_pe), _ptr(seq_lens), B, n_q,
+                              max_seq_len, _ptr(ws), ws_bytes, _ptr(v_acc), n_chunks, flags, _ptr(stream)),
+           "tpla_decode_v")
+
+
+def tpla_project_out(cfg, w, v_acc, R, n_chunks, chunk, ws, ws_bytes, y, out=None, flags=0, group_comm=None, comm=None,
+                     stream=0):
+    _check(_lib.tpla_project_out(C.byref(cfg), C.byref(w), _ptr(v_acc), R, n_chunks, chunk, _ptr(ws), ws_bytes, _ptr(y),
+                                 _ptr(out), flags, group_comm, comm, _ptr(stream)), "tpla_project_out")
 
 
 def tpla_decode_attention(cfg, cache, q_lat, q_pe, seq_lens, B, max_seq_len, ws, ws_bytes, O, lse=None, stream=0):

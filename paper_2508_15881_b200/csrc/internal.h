@@ -89,8 +89,11 @@ cudaError_t launch_combine_seg(const Geom& g, int B, const float* o_part, const 
 
 // K4 + K5a fused (persistent-K3 partials): v[b, h, :] = combine(partials)[b, h, :] · W^UV'_j[h]ᵀ
 bool combine_wuv_supported(const Geom& g);
+// v_acc != null: write (accumulate: add) v in fp32 there instead of bf16 v, column-chunk-major with
+// v_chunks chunks: element (row b, col c) at ((c / kc) * B*n_q + b) * kc + c % kc, kc = H_loc*d_h / v_chunks
 cudaError_t launch_combine_wuv(const Geom& g, int B, int n_q, const float* o_part, const float* ml_part,
-                               const int32_t* meta, const uint16_t* W_UV, uint16_t* v, cudaStream_t s);
+                               const int32_t* meta, const uint16_t* W_UV, uint16_t* v, cudaStream_t s,
+                               float* v_acc = nullptr, bool v_acc_add = false, int v_chunks = 1);
 
 // y_part[ks, b, n] = sum_{k in slice ks} Wt[n, k] * v[b, k]; Wt [N, K] bf16, v [B, K] bf16.
 cudaError_t launch_skinny_gemm(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, int kslices,
@@ -103,13 +106,15 @@ bool wo_tc_supported(int N, int K, int B);
 inline bool wo_blocked(int K) { return K % 64 == 0; }
 size_t wo_tc_part_bytes(int N, int K, int B);
 // out_bf16 (optional): also write bf16(y) (the step's output when no all-reduce follows)
+// [k_begin, k_begin + k_len): a 64-multiple slice of W^O's K rows (k_len 0 = all); v is then [B, k_len],
+// the slice's columns only (a rank projecting its share of a v summed over the latent group)
 cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, void* part_ws, float* y,
-                         bool accumulate, uint16_t* out_bf16, cudaStream_t s);
+                         bool accumulate, uint16_t* out_bf16, cudaStream_t s, int k_begin = 0, int k_len = 0);
 
 // y[b, n] (=|+=) sum_ks y_part[ks, b, n]
 cudaError_t launch_reduce_slices(const float* y_part, int kslices, int B, int N, float* y, bool accumulate,
                                  cudaStream_t s);
 
-cudaError_t launch_cast_bf16(const float* y, long n, uint16_t* out, cudaStream_t s);
+cudaError_t launch_cast_bf16(const float* y, long n, uint16_t* out, cudaStream_t s, const char* name = "C1_cast_bf16");
 
 }  // namespace tpla

@@ -210,9 +210,9 @@ cudaError_t launch_reduce_slices(const float* y_part, int kslices, int B, int N,
   return launch_k(reduce_slices_kernel, blocks, 256, 0, s, y_part, kslices, n, y, accumulate ? 1 : 0);
 }
 
-cudaError_t launch_cast_bf16(const float* y, long n, uint16_t* out, cudaStream_t s) {
+cudaError_t launch_cast_bf16(const float* y, long n, uint16_t* out, cudaStream_t s, const char* name) {
   int blocks = (int)((n / 4 + 255) / 256);
-  KernelScope ks("C1_cast_bf16", s);
+  KernelScope ks(name, s);
   return launch_k(cast_kernel, blocks, 256, 0, s, y, n, out);
 }
 

@@ -25,6 +25,8 @@ struct FArgs {
   uint16_t* v;              // [B * n_q, H_loc * d_h]
   int B, h_loc, w_lat, d_h;
   int n_q;                  // query tokens per sequence: output row b' = b * n_q + i, partial row i * H_loc + h
+  float* v_acc;             // or null: fp32 v written (v_acc_add: added) instead of v, in v_chunks
+  int v_acc_add, v_chunks;  // column chunks [v_chunks][B * n_q][H_loc * d_h / v_chunks]
 };
 
 __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
@@ -122,9 +124,22 @@ __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
         for (int hh = 0; hh < 2; ++hh) {
           const int b = m0 + mw * 16 + (lane >> 2) + hh * 8;
           const int e = nw * 32 + ni * 8 + (lane & 3) * 2;
-          if (b < a.B * a.n_q)
-            *reinterpret_cast<uint32_t*>(a.v + (long)b * a.h_loc * a.d_h + h * a.d_h + e) =
-                pack_bf16(acc[ni][2 * hh], acc[ni][2 * hh + 1]);
+          if (b < a.B * a.n_q) {
+            if (a.v_acc) {                          // (each element has exactly one writer: no atomics)
+              const int kc = a.h_loc * a.d_h / a.v_chunks, c = h * a.d_h + e;   // (kc even: e, c even)
+              const long idx = (long(c / kc) * a.B * a.n_q + b) * kc + c % kc;
+              float2 o = make_float2(acc[ni][2 * hh], acc[ni][2 * hh + 1]);
+              if (a.v_acc_add) {
+                const float2 p = *reinterpret_cast<const float2*>(a.v_acc + idx);
+                o.x += p.x;
+                o.y += p.y;
+              }
+              *reinterpret_cast<float2*>(a.v_acc + idx) = o;
+            } else {
+              const long idx = (long)b * a.h_loc * a.d_h + h * a.d_h + e;
+              *reinterpret_cast<uint32_t*>(a.v + idx) = pack_bf16(acc[ni][2 * hh], acc[ni][2 * hh + 1]);
+            }
+          }
         }
     }
     __syncthreads();
@@ -136,8 +151,9 @@ __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
 bool combine_wuv_supported(const Geom& g) { return g.d_h % 32 == 0 && g.w_lat % 64 == 0 && g.w_lat <= 512; }
 
 cudaError_t launch_combine_wuv(const Geom& g, int B, int n_q, const float* o_part, const float* ml_part,
-                               const int32_t* meta, const uint16_t* W_UV, uint16_t* v, cudaStream_t s) {
-  FArgs a{o_part, ml_part, meta, W_UV, v, B, g.h_loc, g.w_lat, g.d_h, n_q};
+                               const int32_t* meta, const uint16_t* W_UV, uint16_t* v, cudaStream_t s,
+                               float* v_acc, bool v_acc_add, int v_chunks) {
+  FArgs a{o_part, ml_part, meta, W_UV, v, B, g.h_loc, g.w_lat, g.d_h, n_q, v_acc, v_acc_add ? 1 : 0, v_chunks};
   const size_t smem = size_t(g.d_h + kMB) * (g.w_lat + 8) * 2;
   static bool attr = false;
   if (!attr) {

@@ -33,6 +33,7 @@ struct GArgs {
   float* part;        // [max_segs, B, 128] partial sums
   int32_t* meta;      // [n_tiles, 2] first / last segment id of each row tile
   int N, K, B, n_tiles, k_steps;
+  int k_total, k0;    // K-slice: W^O k-steps [k0, k0 + k_steps) of k_total (v holds only the slice's columns)
 };
 
 template <int NP>
@@ -82,7 +83,8 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     for (int i = 0; i < C::NST && lo + i < hi; ++i) {
       const int u = lo + i;
       mbar_arrive_expect_tx(&full[i], C::STAGE);
-      tma_load_2d(smem + i * C::STAGE, &mapA, 0, u * kTM, &full[i], kEvictFirst);   // blocked: unit u = block u
+      const int rt0 = u / a.k_steps, ks0 = u % a.k_steps;
+      tma_load_2d(smem + i * C::STAGE, &mapA, 0, (rt0 * a.k_total + a.k0 + ks0) * kTM, &full[i], kEvictFirst);
     }
   }
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
@@ -104,9 +106,9 @@ skinny_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         if (g >= C::NST) {   // (the first NST weight blocks were issued before the PDL wait)
           mbar_arrive_expect_tx(&full[st], C::STAGE);
           // weights (blocked layout: tile (rt, ks) is one contiguous 16 KB block), read once
-          tma_load_2d(dst, &mapA, 0, (rt * a.k_steps + ks) * kTM, &full[st], kEvictFirst);
+          tma_load_2d(dst, &mapA, 0, (rt * a.k_total + a.k0 + ks) * kTM, &full[st], kEvictFirst);
         }
-        tma_load_2d(dst + C::A_BYTES, &mapB, ks * kBK, 0, &full[st], kEvictNormal);    // v: re-read per tile
+        tma_load_2d(dst + C::A_BYTES, &mapB, ks * kBK, 0, &full[st], kEvictNormal);   // v: re-read per tile
       }
       __syncwarp();
       if (++ks == a.k_steps) { ks = 0; ++rt; }
@@ -251,7 +253,7 @@ bool wo_tc_supported(int N, int K, int B) {
   return K % kBK == 0 && B >= 1 && B <= 256 && N >= 1 && units * 1024 < (1L << 31);   // c*U fits an int
 }
 
-int wo_tc_ctas(int N, int K) {
+int wo_tc_ctas(int N, int K) {   // (K: the columns this launch reduces over)
   const long units = long((N + kTM - 1) / kTM) * (K / kBK);
   return int(std::max(1L, std::min<long>(sm_count(), units)));
 }
@@ -262,18 +264,20 @@ size_t wo_tc_part_bytes(int N, int K, int B) {
 }
 
 cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, void* part_ws, float* y,
-                         bool accumulate, uint16_t* out_bf16, cudaStream_t s) {
+                         bool accumulate, uint16_t* out_bf16, cudaStream_t s, int k_begin, int k_len) {
+  if (k_len <= 0) k_len = K;
   const int n_tiles = (N + kTM - 1) / kTM;
   const int NP = B <= 32 ? 32 : B <= 64 ? 64 : B <= 128 ? 128 : 256;
   CUtensorMap mA, mB;
   // A: the blocked weights viewed as [n_tiles * k_steps * 128 rows, 64 cols]
-  if (!make_map(&mA, Wt, kBK, long(n_tiles) * (K / kBK) * kTM, kBK, kTM) || !make_map(&mB, v, K, B, kBK, NP))
+  if (!make_map(&mA, Wt, kBK, long(n_tiles) * (K / kBK) * kTM, kBK, kTM) || !make_map(&mB, v, k_len, B, kBK, NP))
     return cudaErrorInvalidValue;
   GArgs a;
   a.part = static_cast<float*>(part_ws);
-  const int n_cta = wo_tc_ctas(N, K);
+  const int n_cta = wo_tc_ctas(N, k_len);
   a.meta = reinterpret_cast<int32_t*>(static_cast<char*>(part_ws) + size_t(n_cta + n_tiles) * B * kTM * 4);
-  a.N = N; a.K = K; a.B = B; a.n_tiles = n_tiles; a.k_steps = K / kBK;
+  a.N = N; a.K = K; a.B = B; a.n_tiles = n_tiles; a.k_steps = k_len / kBK;
+  a.k_total = K / kBK; a.k0 = k_begin / kBK;
   cudaError_t e;
   switch (NP) {
     case 32: e = launch_np<32>(mA, mB, a, n_cta, s); break;

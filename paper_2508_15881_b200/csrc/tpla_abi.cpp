@@ -151,6 +151,8 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -171,9 +173,11 @@ bool load_nccl() {
   g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
   g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
   g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.ReduceScatter = (decltype(g_nccl.ReduceScatter))dlsym(h, "ncclReduceScatter");
   g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
-  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy && g_nccl.GetErrorString;
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.ReduceScatter &&
+             g_nccl.CommDestroy && g_nccl.GetErrorString;
   return g_nccl.ok;
 }
 
@@ -580,6 +584,93 @@ tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const
   if (out && !out_done) {
     e = launch_cast_bf16(y, long(R) * g.D, static_cast<uint16_t*>(out), s);
     if (e != cudaSuccess) return cuda_fail(e, "cast");
+  }
+  return ok();
+}
+
+tpla_status tpla_decode_v(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache, const void* q_nope,
+                          const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t n_q, int32_t max_seq_len,
+                          void* ws, size_t ws_bytes, float* v_acc, int32_t n_chunks, int32_t flags, void* stream) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return st;
+  if ((st = check_decode_common(g, cache, q_pe, seq_lens, B, max_seq_len))) return st;
+  if (!w || !w->W_UK || !w->W_UV) return fail(TPLA_ERR_INVALID_ARG, "NULL weights");
+  if (!q_nope || !v_acc || !ws) return fail(TPLA_ERR_INVALID_ARG, "NULL q_nope/v_acc/ws");
+  if (!aligned16(q_nope) || !aligned16(ws) || !aligned16(v_acc)) return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
+  if (n_q < 1 || !(use_tc_attention(g, B) && combine_wuv_supported(g) && n_q * g.h_loc <= 128))
+    return fail(TPLA_ERR_UNSUPPORTED, "tpla_decode_v needs the tcgen05 path (n_q=%d, H_loc=%d)", n_q, g.h_loc);
+  if (n_chunks < 1 || (g.h_loc * g.d_h) % (64 * n_chunks))
+    return fail(TPLA_ERR_DIVISIBILITY, "n_chunks=%d: 64*n_chunks must divide H_loc*d_h=%d", n_chunks, g.h_loc * g.d_h);
+  WsLayout L = ws_layout(g, B, n_q, max_seq_len);
+  if (ws_bytes < L.total) return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, L.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(ws);
+  auto* q_lat = reinterpret_cast<uint16_t*>(base + L.q_lat);
+  auto* o_part = reinterpret_cast<float*>(base + L.o_part);
+  auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
+  auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
+  const auto* qn = static_cast<const uint16_t*>(q_nope);
+  cudaError_t e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK),
+                                   qn + size_t(g.head_begin) * g.d_h, long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h,
+                                   B * n_q, q_lat, true, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K2 absorb_q");
+  e = launch_decode_attn_tc(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, n_q, L.n_cta, o_part,
+                            ml_part, meta, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K3 decode attention");
+  e = launch_combine_wuv(g, B, n_q, o_part, ml_part, meta, static_cast<const uint16_t*>(w->W_UV), nullptr, s, v_acc,
+                         (flags & TPLA_DECODE_ACCUMULATE) != 0, n_chunks);
+  if (e != cudaSuccess) return cuda_fail(e, "K4+K5a combine/W_UV");
+  return ok();
+}
+
+tpla_status tpla_project_out(const tpla_config* cfg, const tpla_weights* w, float* v_acc, int32_t R, int32_t n_chunks,
+                             int32_t chunk, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,
+                             tpla_comm* group_comm, tpla_comm* comm, void* stream) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return st;
+  if (!w || !w->W_O) return fail(TPLA_ERR_INVALID_ARG, "NULL weights");
+  if (!v_acc || !ws || !y) return fail(TPLA_ERR_INVALID_ARG, "NULL v_acc/ws/y");
+  if (!aligned16(v_acc) || !aligned16(ws) || !aligned16(y) || (out && !aligned16(out)))
+    return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
+  const int K = g.h_loc * g.d_h;
+  if (R < 1 || n_chunks < 1 || chunk < 0 || chunk >= n_chunks)
+    return fail(TPLA_ERR_INVALID_ARG, "R=%d, chunk %d of %d", R, chunk, n_chunks);
+  if (K % (64 * n_chunks))
+    return fail(TPLA_ERR_DIVISIBILITY, "n_chunks=%d: 64*n_chunks must divide H_loc*d_h=%d", n_chunks, K);
+  if (group_comm && (group_comm->world != n_chunks || group_comm->rank != chunk))
+    return fail(TPLA_ERR_INVALID_ARG, "group communicator (rank %d of %d) must be chunk %d of %d", group_comm->rank,
+                group_comm->world, chunk, n_chunks);
+  const int kc = K / n_chunks;
+  if (!wo_tc_supported(g.D, K, R))
+    return fail(TPLA_ERR_UNSUPPORTED, "tpla_project_out needs the tcgen05 W^O path (K=%d, R=%d)", K, R);
+  if (comm && (g.k % comm->world))
+    return fail(TPLA_ERR_INVALID_ARG, "communicator world %d does not divide k=%d", comm->world, g.k);
+  if ((group_comm || comm) && !load_nccl()) return fail(TPLA_ERR_NCCL, "NCCL not loadable");
+  const size_t v_bytes = align256(size_t(R) * kc * 2);
+  if (ws_bytes < v_bytes + wo_tc_part_bytes(g.D, kc, R))
+    return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, v_bytes + wo_tc_part_bytes(g.D, kc, R));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float* v_mine = v_acc + size_t(chunk) * R * kc;                  // chunk c: [R, kc] contiguous
+  if (group_comm && n_chunks > 1) {                                // Σ over the group, chunk c to its rank
+    ncclResult_t r = g_nccl.ReduceScatter(v_acc, v_mine, size_t(R) * kc, ncclFloat32, ncclSum, group_comm->comm, s);
+    if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclReduceScatter: %s", g_nccl.GetErrorString(r));
+  }
+  auto* v16 = static_cast<uint16_t*>(ws);
+  cudaError_t e = launch_cast_bf16(v_mine, long(R) * kc, v16, s, "K5_v_cast");           // v = bf16(Σ_j v_j), this slice
+  if (e != cudaSuccess) return cuda_fail(e, "v cast");
+  uint16_t* out16 = comm ? nullptr : static_cast<uint16_t*>(out);
+  e = launch_wo_tc(static_cast<const uint16_t*>(w->W_O), v16, g.D, K, R, static_cast<char*>(ws) + v_bytes, y,
+                   (flags & TPLA_DECODE_ACCUMULATE) != 0, out16, s, chunk * kc, kc);
+  if (e != cudaSuccess) return cuda_fail(e, "K5b W_O (tcgen05)");
+  if (comm) {                                                      // C1: O = AllReduce(Σ Õ)
+    ncclResult_t r = g_nccl.AllReduce(y, y, size_t(R) * g.D, ncclFloat32, ncclSum, comm->comm, s);
+    if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
+    if (out) {
+      e = launch_cast_bf16(y, long(R) * g.D, static_cast<uint16_t*>(out), s);
+      if (e != cudaSuccess) return cuda_fail(e, "cast");
+    }
   }
   return ok();
 }

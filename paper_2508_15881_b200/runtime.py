@@ -49,6 +49,48 @@ def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
     return int(s.cuda_stream)
 
 
+@dataclasses.dataclass(frozen=True)
+class HeadBlockGroup:
+    """One head block i as seen by one process.
+
+    The g ranks {j·(k/g) + i} of head block i share W^O rows; the process holds `local_ranks`
+    of them (they add into one v_acc), and `procs` are the processes holding any of them: v_acc
+    is split into len(procs) column chunks, reduce-scattered over those processes, and this
+    process projects chunk `chunk`."""
+    head_block: int
+    local_ranks: tuple
+    procs: tuple
+    chunk: int
+
+    @property
+    def n_chunks(self) -> int:
+        return len(self.procs)
+
+
+def head_block_groups(k: int, g: int, n_proc: int, proc: int) -> list[HeadBlockGroup]:
+    """Head-block groups of process `proc` when k ranks (group-major plan: rank r has
+    latent shard r div (k/g), head block r mod (k/g)) are spread over n_proc processes in
+    contiguous runs of k/n_proc ranks (as bench.py assigns them)."""
+    if k % n_proc or k % g:
+        raise ValueError(f"k={k} over {n_proc} processes, g={g}")
+    m, nb = k // n_proc, k // g
+    out = []
+    for i in range(nb):
+        members = [j * nb + i for j in range(g)]
+        procs = tuple(sorted({r // m for r in members}))
+        local = tuple(r for r in members if r // m == proc)
+        if local:
+            out.append(HeadBlockGroup(i, local, procs, procs.index(proc)))
+    return out
+
+
+def group_process_sets(k: int, g: int, n_proc: int) -> list[tuple]:
+    """Every distinct process set that must reduce-scatter (size > 1), in one global order (all
+    processes create the communicators in this order, so overlapping sets cannot deadlock)."""
+    sets = {grp.procs for p in range(n_proc) for grp in head_block_groups(k, g, n_proc, p)}
+    return sorted(s for s in sets if len(s) > 1)
+
+
 class TplaRank:
     """One device's share of a TPLA layer (plan, weights, cache, workspace)."""
 
@@ -124,6 +166,23 @@ class TplaRank:
         abi.tpla_decode_mtp(self.cfg, self.weights, self.cache, q_nope, q_pe, seq_lens, B, n_q, self.max_seq_len,
                             self.ws, self.ws_bytes, y, out, abi.DECODE_ACCUMULATE if accumulate else 0, comm,
                             stream_ptr(stream))
+
+    def decode_v(self, q_nope, q_pe, seq_lens, v_acc, *, n_chunks=1, accumulate=False, stream=None):
+        """K2..K5a into v_acc fp32 [n_chunks, B * n_q, H_loc * d_h / n_chunks] (f2(ii): the latent group
+        sums v and shares one W^O read).  q_nope [B, h_q, d_h] or [B, n_q, h_q, d_h]."""
+        B = int(q_nope.shape[0])
+        n_q = int(q_nope.shape[1]) if q_nope.dim() == 4 else 1
+        abi.tpla_decode_v(self.cfg, self.weights, self.cache, q_nope, q_pe, seq_lens, B, n_q, self.max_seq_len, self.ws,
+                          self.ws_bytes, v_acc, n_chunks, abi.DECODE_ACCUMULATE if accumulate else 0, stream_ptr(stream))
+
+    def v_acc_shape(self, rows: int, n_chunks: int = 1):
+        return (n_chunks, rows, self.plan.h_loc * self.spec.d_h // n_chunks)
+
+    def project_out(self, v_acc, y, out=None, *, chunk=0, accumulate=False, group_comm=None, comm=None, stream=None):
+        """[reduce-scatter v_acc over group_comm], y (+)= bf16(v_acc[chunk]) W^O[chunk's rows], [all-reduce]."""
+        n_chunks, R = int(v_acc.shape[0]), int(v_acc.shape[1])
+        abi.tpla_project_out(self.cfg, self.weights, v_acc, R, n_chunks, chunk, self.ws, self.ws_bytes, y, out,
+                             abi.DECODE_ACCUMULATE if accumulate else 0, group_comm, comm, stream_ptr(stream))
 
     def decode_attention(self, q_lat, q_pe, seq_lens, O, lse=None, *, B: int | None = None, stream=None):
         B = int(q_lat.shape[0]) if B is None else B

@@ -228,9 +228,14 @@ def test_attention_parity_divergent_rescale():
 
 
 # ----------------------------------------------------------------------------- end to end (K1..K5)
-def e2e_case(d, dims, k, g, kind, S_list, *, seed=0, modes=("exact", "sliced"), check_rank_parts=True):
+def e2e_case(d, dims, k, g, kind, S_list, *, seed=0, modes=("exact", "sliced"), check_rank_parts=True, wo="rank"):
     """All k ranks of a (k, g) plan run on this GPU, each accumulating into y (k-shard emulation);
-    compared with the oracle's full step (sum over ranks)."""
+    compared with the oracle's full step (sum over ranks).
+    wo: "rank"   every rank projects its own v_j through W^O (tpla_decode, P:139-141);
+        "shared" the g ranks of a head block add their v_j into one v_acc, projected once (f2(ii));
+        "split"  as if each rank of a group were its own process: v_acc in g column chunks per rank,
+                 the group sum formed here (the reduce-scatter's arithmetic), each rank projecting
+                 its chunk's K-slice of W^O."""
     B = len(S_list)
     xf, sseed, U, U32, alpha = transform_inputs(kind, dims, 21, g)
     basis = U if kind == "pca" else None
@@ -260,9 +265,31 @@ def e2e_case(d, dims, k, g, kind, S_list, *, seed=0, modes=("exact", "sliced"), 
             kp = np.stack([k_pe[b][n_prompt[b] + step] for b in sel])
             r.append(bf16_from_bits(ck, d), bf16_from_bits(kp, d), torch.tensor(sel, dtype=torch.int32, device=d),
                      torch.tensor([n_prompt[b] + step for b in sel], dtype=torch.int32, device=d), abi.RMS_SLICED)
-        r.decode(bf16_from_bits(q, d), bf16_from_bits(qpe, d), torch.tensor(S_list, dtype=torch.int32, device=d),
-                 y, accumulate=True)
+        if wo == "rank":
+            r.decode(bf16_from_bits(q, d), bf16_from_bits(qpe, d), torch.tensor(S_list, dtype=torch.int32, device=d),
+                     y, accumulate=True)
         ranks.append(r)
+    if wo != "rank":
+        lens = torch.tensor(S_list, dtype=torch.int32, device=d)
+        n_ch = 1 if wo == "shared" else g
+        blocks = sorted({r.plan.head_block for r in ranks})
+        for hb in blocks:
+            grp = [r for r in ranks if r.plan.head_block == hb]
+            assert len(grp) == g
+            accs = [torch.full(grp[0].v_acc_shape(B, n_ch), float("nan"), device=d) for _ in range(len(grp))]
+            for j, r in enumerate(grp):
+                if wo == "shared":     # co-located: one accumulator for the group
+                    r.decode_v(bf16_from_bits(q, d), bf16_from_bits(qpe, d), lens, accs[0], accumulate=j > 0)
+                else:
+                    r.decode_v(bf16_from_bits(q, d), bf16_from_bits(qpe, d), lens, accs[j], n_chunks=n_ch)
+            if wo == "shared":
+                grp[0].project_out(accs[0], y, accumulate=True)
+            else:
+                tot = torch.stack(accs).sum(0)
+                for j, r in enumerate(grp):
+                    a = torch.full_like(tot, float("nan"))   # only chunk j is read by rank j
+                    a[j] = tot[j]
+                    r.project_out(a, y, chunk=j, accumulate=True)
     out = torch.empty((B, dims.D), dtype=torch.bfloat16, device=d)
     abi.tpla_sync(0)
     torch.cuda.synchronize()
@@ -301,6 +328,31 @@ def test_e2e_parity_dsv3_shape(k, g, kind):
 
 def test_e2e_parity_kimi_shape():
     e2e_case(dev(), synth.PRESETS["kimi"], 4, 4, "hadamard", [64, 129])
+
+
+@pytest.mark.parametrize("dname,k,g,kind", [("dsv3", 2, 2, "hadamard"), ("dsv3", 4, 2, "pca"), ("dsv3", 8, 8, "hadamard"),
+                                            ("kimi", 8, 4, "hadamard"), ("dsv3", 8, 2, "identity")])
+@pytest.mark.parametrize("wo", ["shared", "split"])
+def test_e2e_parity_group_shared_wo(dname, k, g, kind, wo):
+    """the latent group sums v before one W^O product (co-located or reduce-scattered)."""
+    e2e_case(dev(), synth.PRESETS[dname], k, g, kind, [5, 200, 333], wo=wo)
+
+
+def test_project_out_rejects_bad_chunking():
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    r = TplaRank(spec_of(dims), k=8, g=8, rank=0, batch=2, max_seq_len=64, device=d)
+    w = synth.gen_weights(dims, 1)
+    r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_HADAMARD)
+    y = torch.zeros((2, dims.D), dtype=torch.float32, device=d)
+    v = torch.zeros((3, 2, dims.h_q * dims.d_h // 3 + 1), dtype=torch.float32, device=d)
+    with pytest.raises(abi.TplaError) as ei:            # 3 chunks of 64-multiples do not tile K = 16384
+        r.project_out(v, y, chunk=0)
+    assert ei.value.status == abi.ERR_DIVISIBILITY
+    v = torch.zeros(r.v_acc_shape(2, 2), dtype=torch.float32, device=d)
+    with pytest.raises(abi.TplaError) as ei:
+        r.project_out(v, y, chunk=2)
+    assert ei.value.status == abi.ERR_INVALID_ARG
 
 
 def mtp_case(d, dims, k, g, n_q, S_list, *, seed=0, kind="hadamard"):
@@ -439,6 +491,40 @@ def test_bf16_output_and_nccl_world1():
     out = torch.empty((2, dims.D), dtype=torch.bfloat16, device=d)
     r.decode(bf16_from_bits(q, d), bf16_from_bits(qpe, d), lens, y1, out, comm=comm)
     torch.cuda.synchronize()
+    abi.tpla_comm_destroy(comm)
+    assert torch.equal(y0, y1)
+    assert torch.equal(out, y1.to(torch.bfloat16))
+
+
+def test_decode_v_project_out_nccl_world1_equals_decode():
+    """One rank: tpla_decode_v + tpla_project_out (with 1-rank group and TP communicators: the
+    reduce-scatter and all-reduce call path) is bit-identical to tpla_decode — same bf16 v, same
+    W^O kernel and reduction order."""
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    B, n = 3, 150
+    r = TplaRank(spec_of(dims), k=2, g=2, rank=1, batch=B, max_seq_len=n, device=d)
+    w = synth.gen_weights(dims, 6)
+    r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_HADAMARD, sign_seed=5)
+    ck = bf16_from_bits(np.concatenate([synth.gen_raw_ckv(dims, n, 2, b) for b in range(B)]), d)
+    kp = bf16_from_bits(np.concatenate([synth.gen_kpe(dims, n, 2, b) for b in range(B)]), d)
+    seq = torch.repeat_interleave(torch.arange(B, dtype=torch.int32), n).to(d)
+    pos = torch.arange(n, dtype=torch.int32).repeat(B).to(d)
+    r.append(ck, kp, seq, pos, abi.RMS_SLICED)
+    q, qpe = synth.gen_queries(dims, B, 7)
+    q, qpe = bf16_from_bits(q, d), bf16_from_bits(qpe, d)
+    lens = torch.tensor([n, n - 7, 64], dtype=torch.int32, device=d)
+    y0 = torch.zeros((B, dims.D), dtype=torch.float32, device=d)
+    r.decode(q, qpe, lens, y0)
+    gcomm = abi.tpla_comm_init(abi.tpla_comm_unique_id(), 1, 0)
+    comm = abi.tpla_comm_init(abi.tpla_comm_unique_id(), 1, 0)
+    v = torch.empty(r.v_acc_shape(B), dtype=torch.float32, device=d)
+    r.decode_v(q, qpe, lens, v)
+    y1 = torch.zeros_like(y0)
+    out = torch.empty((B, dims.D), dtype=torch.bfloat16, device=d)
+    r.project_out(v, y1, out, group_comm=gcomm, comm=comm)
+    torch.cuda.synchronize()
+    abi.tpla_comm_destroy(gcomm)
     abi.tpla_comm_destroy(comm)
     assert torch.equal(y0, y1)
     assert torch.equal(out, y1.to(torch.bfloat16))
