@@ -486,7 +486,7 @@ def main():
 
     # ---- roofline of the dominant kernel (K3 attention), per launch = one rank's shard
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
-    k3_name = next((n for n in prof if n.startswith("K3")), None)
+    k3_name = next((n for n in prof if n.startswith("K3_attn")), None)
     plan0 = ranks[0].plan
     bytes_k3 = B * S * plan0.row_width * 2                       # Σ_b S_b · W · 2
     flops_k3 = 2 * B * nq * S * plan0.h_loc * (2 * plan0.w_lat + dims.d_r)   # (MTP: ~S keys per token)

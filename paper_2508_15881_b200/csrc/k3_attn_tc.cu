@@ -76,6 +76,13 @@ constexpr int kTrace = 128;
 constexpr int kSlots = 22;        // trace slots: qk_issue, pv_issue, s_ready, p_done, qk_issued, pv_issued,
                                   // then p_done of each softmax warp 4..11, then the producer's TMA issue,
                                   // then warp 4's softmax phases: S loaded, max exchanged, exps done
+// startup events of the traced CTA (clock64): 0 kernel entry, 1 after pdl_wait, 2 schedule done,
+// 3 producer lookups resolved, 4 first TMA issued, 5 Q loaded (warp 4), 6 MMA saw q_ready,
+// 7 MMA saw kv_full(0)
+#define EV(i)                                                                            \
+  do {                                                                                   \
+    if ((MODE & 2) && blockIdx.x == a.trace_cta) a.trace[kSlots * kTrace + 4 * kMaxCta + (i)] = clock64(); \
+  } while (0)
 #define TRACE(slot, gg)                                                                  \
   do {                                                                                   \
     if ((MODE & 2) && blockIdx.x == a.trace_cta && (gg) < kTrace) a.trace[(slot) * kTrace + (gg)] = clock64(); \
@@ -95,6 +102,15 @@ struct Cfg {
   // once; at W_lat <= 128 the MMA work per 64-token tile is too short to hide those (measured),
   // so the larger tile halves the synchronisation per byte.
   static constexpr int TT = WL <= 128 ? 128 : 64;
+  // PP (ping-pong softmax, TT = 128): the two warps of a TMEM lane quadrant take alternate tiles
+  // with whole rows each, instead of splitting every tile's columns and exchanging row maxima.
+  // They share one SMSP (warps w and w+4); out of phase, one warp's loads, stores and barrier
+  // waits overlap the other's exponentials (see the PP branch of the softmax).
+#ifdef TPLA_NO_PP
+  static constexpr bool PP = false;
+#else
+  static constexpr bool PP = !PAIR && TT == 128;
+#endif
   // S (= P) buffers in TMEM.  Three when they fit (W_lat = 64: O 64 + Q' 32 + 3 x 128 = 480
   // columns): QK then runs two tiles ahead of PV, so S(g+1) is ready when the softmax finishes
   // tile g (with two buffers the softmax waited ~470 cycles per tile for it, measured).
@@ -163,6 +179,7 @@ template <int W_LAT, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   pdl_trigger();
+  if (threadIdx.x == 0) EV(0);
   using C = Cfg<W_LAT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -179,6 +196,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   __shared__ int s_before;
   __shared__ float red_max[C::NSB][2][128];   // [S buffer][half][row] partial row maxima
   __shared__ float red_l[2][128];        // [half][row] partial row sums at a segment end
+  __shared__ float red_m[2][128];        // PP: [set][row] the max each set's sums are expressed in
+  __shared__ float m_row[128];           // PP: the row's running max after the last finalised tile
   __shared__ uint64_t x_full[8], x_ok[8]; // PAIR, per softmax warp: peer's logits landed / peer read ours
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -190,7 +209,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap);
     for (int i = 0; i < C::NST; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
-    for (int i = 0; i < C::NSB; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 8); mbar_init(&pv_done[i], 1); }
+    for (int i = 0; i < C::NSB; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], C::PP ? 4 : 8); mbar_init(&pv_done[i], 1); }
     mbar_init(&q_ready, 8);      // p_full / q_ready: one arrival per softmax warp (elected lane)
     if (C::PAIR)
       for (int i = 0; i < 8; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_ok[i], 1); }
@@ -200,6 +219,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
   if (tid == 0) s_before = 0;
   pdl_wait();   // everything below reads the predecessors' outputs (seq_lens, Q', cache rows)
+  if (threadIdx.x == 0) EV(1);
   if (warp == 3) {
     // tiles per sequence -> exclusive prefix sum (warp scan, 32 sequences per step)
     int carry = 0;
@@ -242,7 +262,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if ((MODE & 2) && tid == 0) a.trace[kSlots * kTrace + 2 * c] = globaltimer();
+  if ((MODE & 2) && tid == 0) {
+    a.trace[kSlots * kTrace + 2 * c] = globaltimer();
+    a.trace[kSlots * kTrace + 2 * kMaxCta + 2 * c] = clock64();
+  }
   const uint32_t tb = tmem_base;
   Sched S;
   S.lo = lo_arr[c];
@@ -269,7 +292,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       if (tok >= slen[bb]) tok = tok0;
       return a.block_table[(long)bb * a.max_pages + tok / a.page_size] * a.page_size + tok % a.page_size;
     };
+    if (lane == 0) EV(2);
     int rows_cur = lookup(lane), rows_next = lookup(32 + lane);
+    if (__shfl_sync(0xffffffffu, rows_cur + rows_next, 0) >= 0 && lane == 0) EV(3);
     for (int t = S.lo, g = 0; t < S.hi; ++t, ++g) {
       const int u0 = g * C::SUB;                       // SUB divides 32: a tile never spans batches
       if (u0 > 0 && (u0 & 31) == 0) {
@@ -283,6 +308,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       mbar_wait(&kv_empty[st], ((g / C::NST) & 1) ^ 1);
       if (elect_one()) {
         TRACE(14, g);
+        if (g == 0) EV(4);
         uint8_t* dst = s_kv + st * C::STAGE_BYTES;
         if (MODE & 4) {
           mbar_arrive(&kv_full[st]);      // diagnostic: no HBM traffic, stale smem contents
@@ -345,10 +371,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
       const int g0 = g;
       mbar_wait(&q_ready, seg & 1);
+      if (seg == 0 && lane == 0) EV(6);
       tc_fence_after();
       for (int t = t0; t < t1; ++t, ++g) {
         const int st = g % C::NST;
         mbar_wait(&kv_full[st], (g / C::NST) & 1);
+        if (g == 0 && lane == 0) EV(7);
         tc_fence_after();
         if (elect_one()) {
           TRACE(0, g);
@@ -423,7 +451,186 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&q_ready);
+        if (warp == 4 && lane == 0 && bb == S.b_first) EV(5);
     };
+    if constexpr (C::PP) {
+    // ---- ping-pong softmax (TT = 128).  Warp set `half` takes the tiles with g % 2 == half, whole
+    // 128-column rows.  A tile's exponentials use a provisional running max read from m_row
+    // (the max the previous tile's warp published) — no max pass; the tiles are then finalised in
+    // order (named barriers between the two warps of the quadrant): if the provisional max turns
+    // out stale, or a row's tile sum leaves [0, 2^20] (p may exceed 2^20 only when the max grew:
+    // the lazy-rescale condition, with inf/NaN caught by the same test), the tile's logits (still
+    // in TMEM: P is stored only after finalising) are reloaded and redone with the exact rule.
+    // The first tile of a segment takes its exact row max.
+    const uint32_t fin_mine = 5 + 2 * q4 + half, fin_other = 5 + 2 * q4 + (half ^ 1);
+    constexpr float kLim = 1048576.f;                   // 2^20
+    volatile float* mrow = m_row;
+    auto row_max = [&](const float* x) {
+      float m0 = x[0], m1 = x[1], m2 = x[2], m3 = x[3];
+#pragma unroll
+      for (int j = 4; j < C::TT; j += 4) {
+        m0 = fmaxf(m0, x[j]); m1 = fmaxf(m1, x[j + 1]); m2 = fmaxf(m2, x[j + 2]); m3 = fmaxf(m3, x[j + 3]);
+      }
+      return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+    };
+    // p = 2^(x·sc − m) for the row's 128 columns -> bf16 pairs pw, and the row's tile sum
+    auto exps = [&](const float* x, float m, uint32_t (&pw)[C::TT / 2]) {
+      const float neg_m = m == -INFINITY ? 0.f : -m;    // (a row with nothing visible: p = 0)
+      const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(neg_m, neg_m);
+      uint64_t l01 = f2_pack(0.f, 0.f), l23 = f2_pack(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < C::TT / 2; j += 2) {
+        float y0, y1, y2, y3;
+        f2_unpack(ffma2(f2_pack(x[2 * j], x[2 * j + 1]), sc2, nm2), y0, y1);
+        f2_unpack(ffma2(f2_pack(x[2 * j + 2], x[2 * j + 3]), sc2, nm2), y2, y3);
+        const float p0 = ex2(y0), p1 = ex2(y1);
+        float p2, p3;
+        if (kPolyEvery<W_LAT> > 0 && (j / 2) % kPolyEvery<W_LAT> == 0) {
+          ex2_poly2<true>(y2, y3, p2, p3);
+        } else {
+          p2 = ex2(y2);
+          p3 = ex2(y3);
+        }
+        l01 = fadd2(l01, f2_pack(p0, p1));
+        l23 = fadd2(l23, f2_pack(p2, p3));
+        pw[j] = pack_bf16x2(p0, p1);
+        pw[j + 1] = pack_bf16x2(p2, p3);
+      }
+      float a0, a1, a2, a3;
+      f2_unpack(l01, a0, a1);
+      f2_unpack(l23, a2, a3);
+      return (a0 + a1) + (a2 + a3);
+    };
+    int g = 0, seg = 0;
+    if (S.b_first <= S.b_last) load_q(S.b_first);
+    for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
+      const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
+      const int S_b = slen[b] + len_adj;                 // this row's visible length
+      float m_w = -INFINITY;                             // the max this warp's sum l_w is expressed in
+      float l_w = 0.f;
+      for (int t = t0; t < t1; ++t, ++g) {
+        if ((g & 1) != half) continue;
+        const int sb = g % C::NSB;
+        if (q4 == 0 && lane == 0) TRACE(18, g);
+        mbar_wait(&s_full[sb], (g / C::NSB) & 1);
+        if (q4 == 0 && lane == 0) TRACE(2, g);
+        if (!q_active) {                                 // no head rows here: P stays 0 (S rows are 0)
+          if (lane == 0) mbar_arrive(&p_full[sb]);
+          continue;
+        }
+        tc_fence_after();
+        const uint32_t s_addr = lane_base + C::S_COL0 + sb * C::TT;
+        uint32_t sv[C::TT / 32][32];
+        float* x = reinterpret_cast<float*>(&sv[0][0]);
+        const int nvalid = S_b - (t - cum[b]) * C::TT;   // (per row when n_q > 1)
+        auto load_s = [&]() {
+#pragma unroll
+          for (int q = 0; q < C::TT / 32; ++q) tmem_ld32(s_addr + 32 * q, sv[q]);
+          tmem_ld_wait();
+          if (nvalid < C::TT) {                          // ragged last tile of the sequence
+#pragma unroll
+            for (int j = 0; j < C::TT; ++j) x[j] = j < nvalid ? x[j] : -INFINITY;
+          }
+        };
+        load_s();
+        if (q4 == 0 && lane == 0) TRACE(15, g);
+        const float m_prov = t == t0 ? row_max(x) * sc : mrow[r];   // sc > 0: max commutes with scaling
+        uint32_t pw[C::TT / 2];
+        float ts = exps(x, m_prov, pw);
+        if (q4 == 0 && lane == 0) TRACE(16, g);
+        // ---- finalise in tile order: tile g-1 (the other warp) has published its final max
+        if (t > t0) named_bar_sync(fin_other, 64);
+        if (q4 == 0 && lane == 0) TRACE(17, g);
+        const float m_prev = t > t0 ? mrow[r] : -INFINITY;
+        const bool redo = !(ts <= kLim) || (t > t0 && m_prov != m_prev);
+        float m_fin = m_prov;
+        if (__any_sync(0xffffffffu, redo)) {             // rare: reload the logits, exact rule
+          load_s();
+          const float mx = row_max(x) * sc;
+          if (redo) m_fin = mx > m_prev + kRescaleThreshold ? mx : m_prev;
+          ts = exps(x, m_fin, pw);
+        }
+        // O holds PV(g-1) and earlier at m_prev: rescale the rows whose max grew (warp-collective)
+        const bool grow = t > t0 && m_fin != m_prev;
+        if (__any_sync(0xffffffffu, grow)) {
+          const float f = grow ? ex2(m_prev - m_fin) : 1.f;
+          mbar_wait(&pv_done[(g - 1) % C::NSB], ((g - 1) / C::NSB) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c0 = 0; c0 < C::WL; c0 += 32) {
+            uint32_t ov[32];
+            tmem_ld32(lane_base + C::O_COL + c0, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * f);
+            tmem_st32(lane_base + C::O_COL + c0, ov);
+          }
+        }
+        mrow[r] = m_fin;
+        if (m_fin != m_w) {                              // this warp's sum follows the row's max
+          l_w = m_w == -INFINITY ? 0.f : l_w * ex2(m_w - m_fin);
+          m_w = m_fin;
+        }
+        l_w += ts;
+        // P (bf16 pairs) over columns [0, TT/2) of S(g)
+#pragma unroll
+        for (int q = 0; q < C::TT / 64; ++q) {
+          uint32_t (&pq)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pw[32 * q]);
+          tmem_st32(s_addr + 32 * q, pq);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        if (q4 == 0 && lane == 0) TRACE(3, g);
+        if (lane == 0) TRACE(6 + warp - 4, g);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[sb]);
+        if (t + 1 < t1) {                                // the other warp finalises tile g+1 next
+          __threadfence_block();
+          named_bar_arrive(fin_mine, 64);
+        }
+      }
+      // Stage the next segment's Q once the segment's last QK is complete (the other warp may
+      // have consumed that S), so its first QKs overlap this epilogue.
+      mbar_wait(&s_full[(g - 1) % C::NSB], ((g - 1) / C::NSB) & 1);
+      tc_fence_after();
+      if (b < S.b_last) load_q(b + 1);
+      if (!q_active) continue;
+      // ---- epilogue of the segment: unnormalised partial (O, m, l); the two sets' sums meet
+      red_l[half][r] = l_w;
+      red_m[half][r] = m_w;
+      mbar_wait(&pv_done[(g - 1) % C::NSB], ((g - 1) / C::NSB) & 1);
+      tc_fence_after();
+      named_bar_sync(pair_bar, 64);
+      const float m_o = red_m[half ^ 1][r], l_o = red_l[half ^ 1][r];
+      const float m_seg = fmaxf(m_w, m_o);              // the last tile's max (maxima only grow)
+      const float l = (m_w == -INFINITY ? 0.f : l_w * ex2(m_w - m_seg)) +
+                      (m_o == -INFINITY ? 0.f : l_o * ex2(m_o - m_seg));
+      const int seg_id = S.seg_base + seg;
+      {
+        float* op = a.o_part + ((long)seg_id * n_rows + r) * W_LAT;
+#pragma unroll 1
+        for (int c0 = half * (C::WL / 2); c0 < (half + 1) * (C::WL / 2); c0 += 32) {
+          uint32_t ov[32];
+          tmem_ld32(lane_base + C::O_COL + c0, ov);
+          tmem_ld_wait();
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(op + c0 + j) = make_float4(__uint_as_float(ov[j]), __uint_as_float(ov[j + 1]),
+                                                                    __uint_as_float(ov[j + 2]), __uint_as_float(ov[j + 3]));
+          }
+        }
+        if (row_ok && half == 0) {
+          a.ml_part[((long)seg_id * n_rows + r) * 2] = m_seg;
+          a.ml_part[((long)seg_id * n_rows + r) * 2 + 1] = l;
+        }
+      }
+      if (r == 0 && half == 0 && t0 == cum[b]) a.meta[2 * b] = seg_id;
+      if (r == 0 && half == 0 && t1 == cum[b + 1]) a.meta[2 * b + 1] = seg_id;
+      named_bar_sync(pair_bar, 64);                     // red_l / red_m free again
+      tc_fence_before();
+    }
+    } else {
     int g = 0, seg = 0;
     int xk = 0;                                          // PAIR: logit exchanges done by this warp
     if (S.b_first <= S.b_last) load_q(S.b_first);
@@ -619,12 +826,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       named_bar_sync(pair_bar, 64);                     // red_l free again
       tc_fence_before();
     }
+    }
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if ((MODE & 2) && tid == 0) a.trace[kSlots * kTrace + 2 * c + 1] = globaltimer();
+  if ((MODE & 2) && tid == 0) {
+    a.trace[kSlots * kTrace + 2 * c + 1] = globaltimer();
+    a.trace[kSlots * kTrace + 2 * kMaxCta + 2 * c + 1] = clock64();
+  }
   if (C::PAIR) cluster_sync();   // the peer may still be writing into our smem / arriving on our barriers
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tb);
 }
@@ -718,7 +929,7 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
   if (mode && strncmp(mode, "trace", 5) == 0) {   // trace, trace_notma, trace_nold
     static long long* buf = nullptr;
     const int nb = kSlots * kTrace + 2 * n_cta;
-    if (!buf) cudaMalloc(&buf, (kSlots * kTrace + 2 * kMaxCta) * sizeof(long long));
+    if (!buf) cudaMalloc(&buf, (kSlots * kTrace + 4 * kMaxCta + 16) * sizeof(long long));
     TcArgs b = a;
     b.trace = buf;
     const char* tc = getenv("TPLA_K3_TRACE_CTA");
@@ -726,10 +937,12 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
     cudaError_t e = strcmp(mode, "trace_notma") == 0 ? launch_tc_mode<W_LAT, 6>(map, b, n_cta, s)
                     : strcmp(mode, "trace_nold") == 0  ? launch_tc_mode<W_LAT, 10>(map, b, n_cta, s)
                                                         : launch_tc_mode<W_LAT, 2>(map, b, n_cta, s);
-    static long long h[kSlots * kTrace + 2 * kMaxCta];
+    static long long h[kSlots * kTrace + 4 * kMaxCta + 16];
     cudaStreamSynchronize(s);
-    cudaMemcpy(h, buf, nb * sizeof(long long), cudaMemcpyDeviceToHost);
+    cudaMemcpy(h, buf, (kSlots * kTrace + 4 * kMaxCta + 16) * sizeof(long long), cudaMemcpyDeviceToHost);
+    (void)nb;
     const long long* cs = h + kSlots * kTrace;
+    const long long* cc = cs + 2 * kMaxCta;        // clock64 at the same two points
     long long t0 = cs[0], t1 = 0, s_max = 0;
     for (int c = 0; c < n_cta; ++c) {
       t0 = std::min(t0, cs[2 * c]);
@@ -738,9 +951,19 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
     for (int c = 0; c < n_cta; ++c) {
       long long st = cs[2 * c] - t0, en = cs[2 * c + 1] - t0;
       s_max = std::max(s_max, st);
-      if (c % 8 == 0) fprintf(stderr, "[k3 cta] %3d start %6lld ns end %6lld ns\n", c, st, en);
+      if (c % 8 == 0 || c == b.trace_cta)
+        fprintf(stderr, "[k3 cta] %3d start %6lld ns end %6lld ns  %lld cycles (%.0f MHz)\n", c, st, en,
+                cc[2 * c + 1] - cc[2 * c], 1e3 * double(cc[2 * c + 1] - cc[2 * c]) / double(en - st));
     }
     fprintf(stderr, "[k3 cta] span %lld ns, latest start %lld ns\n", t1 - t0, s_max);
+    fprintf(stderr, "[k3 cta] traced CTA: start -> qk_issue[0] %lld cycles, qk_issue[0] -> end %lld cycles\n",
+            h[0] - cc[2 * b.trace_cta], cc[2 * b.trace_cta + 1] - h[0]);
+    {
+      const long long* ev = h + kSlots * kTrace + 4 * kMaxCta;
+      fprintf(stderr, "[k3 start] cycles from kernel entry: pdl_wait %lld, sched %lld, lookups %lld, tma0 %lld, "
+              "q_loaded %lld, mma_q %lld, mma_kv0 %lld, qk0 %lld\n", ev[1] - ev[0], ev[2] - ev[0], ev[3] - ev[0],
+              ev[4] - ev[0], ev[5] - ev[0], ev[6] - ev[0], ev[7] - ev[0], h[0] - ev[0]);
+    }
     fprintf(stderr, "[k3 trace] g qk_issue qk_issued s_ready p_done pv_issue pv_issued (cycles rel. to qk_issue[0])\n");
     for (int g = 0; g < kTrace; ++g)
       fprintf(stderr, "[k3 trace] %3d %8lld %8lld %8lld %8lld %8lld %8lld\n", g, h[g] - h[0], h[4 * kTrace + g] - h[0],

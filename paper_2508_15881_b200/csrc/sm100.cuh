@@ -213,6 +213,10 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
+// signal (no wait) on a named barrier that other threads bar.sync on (producer -> consumer)
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -320,9 +324,16 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
 // error 7.5e-5, far below the bf16 rounding P gets), and j added into the exponent field.
 // x is clamped at -126.5 so that j >= -126: 2^f < 1 has biased exponent 126, and 126 + j must
 // not go negative (below that the result is a denormal ~1e-38, i.e. 0 next to P's 2^-8 floor).
+// kHi: also clamp from above (at 2^64), for inputs not bounded by a known max — the result must
+// then stay a large finite value rather than wrap the exponent field
+template <bool kHi = false>
 __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& p0, float& p1) {
   x0 = fmaxf(x0, -126.5f);
   x1 = fmaxf(x1, -126.5f);
+  if (kHi) {
+    x0 = fminf(x0, 64.f);
+    x1 = fminf(x1, 64.f);
+  }
   const uint64_t magic = f2_pack(12582912.f, 12582912.f);
   const uint64_t x = f2_pack(x0, x1);
   const uint64_t t = fadd2(x, magic);                                  // low mantissa bits: round(x)

@@ -23,6 +23,17 @@ __global__ void rate_kernel(float* out, long long* cyc) {
         uint32_t u = __float_as_uint(v[i]);
         asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(u));
         v[i] = __uint_as_float(u);
+      } else if (OP == 4) { // cvt.rn.bf16x2.f32 (F2FP.BF16.F32.PACK_AB): is it on the MUFU pipe?
+        uint32_t u;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(u) : "f"(v[i]), "f"(v[(i + 1) & 7]));
+        v[i] = __uint_as_float(u) * 0.5f;
+      } else if (OP == 5) { // one ex2 + one cvt per element (the softmax's mix)
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[i]));
+        uint32_t u;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(u) : "f"(v[i]), "f"(v[(i + 3) & 7]));
+        v[(i + 5) & 7] += __uint_as_float(u);
+      } else if (OP == 6) { // fmax only
+        asm volatile("max.f32 %0, %0, %1;" : "+f"(v[i]) : "f"(v[(i + 1) & 7]));
       } else {              // ex2.approx.ftz.bf16x2
         uint32_t u = __float_as_uint(v[i]);
         asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(u));
@@ -64,6 +75,9 @@ int main() {
   for (int t : {128, 256, 1024}) run<1>("ffma", t);
   for (int t : {256, 1024}) run<2>("ex2.f16x2 (instr)", t);
   for (int t : {256, 1024}) run<3>("ex2.bf16x2 (instr)", t);
+  for (int t : {256, 1024}) run<4>("cvt.bf16x2 (instr)", t);
+  for (int t : {256, 1024}) run<5>("ex2+cvt (pairs)", t);
+  for (int t : {256, 1024}) run<6>("fmax", t);
   printf("MUFU OK\n");
   return 0;
 }
