@@ -73,9 +73,11 @@ struct TcArgs {
   int trace_cta;
 };
 constexpr int kTrace = 128;
-constexpr int kSlots = 22;        // trace slots: qk_issue, pv_issue, s_ready, p_done, qk_issued, pv_issued,
+constexpr int kSlots = 23;        // trace slots: qk_issue, pv_issue, s_ready, p_done, qk_issued, pv_issued,
                                   // then p_done of each softmax warp 4..11, then the producer's TMA issue,
-                                  // then warp 4's softmax phases: S loaded, max exchanged, exps done
+                                  // then warp 4's softmax phases: S loaded, max exchanged, exps done,
+                                  // MMA warp waits (19-21, non-PAIR), slot 22: tile landed (kv_full
+                                  // observed by the otherwise idle warp 3)
 // startup events of the traced CTA (clock64): 0 kernel entry, 1 after pdl_wait, 2 schedule done,
 // 3 producer lookups resolved, 4 first TMA issued, 5 Q loaded (warp 4), 6 MMA saw q_ready,
 // 7 MMA saw kv_full(0)
@@ -172,6 +174,8 @@ __device__ __forceinline__ int upper_bound_cum(const int* cum, int n, int x) {  
 
 // MODE 0: the kernel.  MODE 1 (diagnostic, TPLA_K3_MODE=stream): the TMA ring alone — every
 // tile is released as soon as it lands, no MMA/softmax — to measure the cache streaming rate.
+// Bit 16 (nosm, PP only): the softmax warps pass every tile straight through (MMA + ring alone).
+// Bit 32 (nomma): the MMA warp commits without issuing MMAs (softmax + ring alone).
 // MODE bit 2 (trace): per-tile clock64 stamps.  Bit 8 (nold): softmax without its TMEM
 // loads/stores.  Bit 4 (notma): no cache loads (stale smem), to time MMA + softmax alone.  Diagnostic modes
 // compute garbage; they exist to isolate the pipeline's limiter.
@@ -340,6 +344,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         if (min(S.hi, cum[b + 1]) == cum[b + 1]) a.meta[2 * b + 1] = S.seg_base + seg;
       }
     }
+  } else if ((MODE & 2) && warp == 3) {
+    // trace only: observe when each tile lands (the MMA warp sees kv_full only when it gets to it)
+    if (blockIdx.x == a.trace_cta)
+      for (int g = 0; g < S.hi - S.lo && g < kTrace; ++g) {
+        while (!mbar_try_wait(&kv_full[g % C::NST], (g / C::NST) & 1)) {
+        }
+        if (lane == 0) TRACE(22, g);
+      }
   } else if (warp == 1) {
     // ============================================================ MMA issuer (converged warp, one issuer)
     constexpr uint32_t id_qk = idesc_bf16(128, C::TT, false, false);
@@ -350,6 +362,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     int g = 0, seg = 0;
     auto issue_pv = [&](int gp, bool first_pv) {
       const int st = gp % C::NST;
+      if (!C::PAIR && lane == 0) TRACE(21, gp);
       mbar_wait(&p_full[gp % C::NSB], (gp / C::NSB) & 1);
       tc_fence_after();
       if (elect_one()) {
@@ -359,8 +372,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         const uint32_t p_tmem = tb + C::S_COL0 + (gp % C::NSB) * C::TT;
 #pragma unroll
         for (int kk = 0; kk < C::TT / 16; ++kk)      // 16 tokens (2 KB of rows) per step
-          mma_ts(tb + C::O_COL, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), id_pv,
-                 (first_pv && kk == 0) ? 0u : 1u);
+          if (!(MODE & 32))
+            mma_ts(tb + C::O_COL, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), id_pv,
+                   (first_pv && kk == 0) ? 0u : 1u);
         mma_commit(&kv_empty[st]);
         mma_commit(&pv_done[gp % C::NSB]);
         TRACE(5, gp);
@@ -375,7 +389,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       tc_fence_after();
       for (int t = t0; t < t1; ++t, ++g) {
         const int st = g % C::NST;
+        if (!C::PAIR && lane == 0) TRACE(19, g);
         mbar_wait(&kv_full[st], (g / C::NST) & 1);
+        if (!C::PAIR && lane == 0) TRACE(20, g);
         if (g == 0 && lane == 0) EV(7);
         tc_fence_after();
         if (elect_one()) {
@@ -384,14 +400,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           const uint32_t s_tmem = tb + C::S_COL0 + (g % C::NSB) * C::TT;
 #pragma unroll
           for (int kk = 0; kk < C::WL / 16; ++kk)     // Q'_j (TMEM) x ĉ tileᵀ: box kk/4, +32 B per k-step
-            mma_ts(s_tmem, tb + C::Q_COL + kk * 8,
-                   kv_desc + uint64_t(((kk >> 2) * C::BOX_BYTES + (kk & 3) * 32) >> 4), id_qk, kk > 0 ? 1u : 0u);
+            if (!(MODE & 32))
+              mma_ts(s_tmem, tb + C::Q_COL + kk * 8,
+                     kv_desc + uint64_t(((kk >> 2) * C::BOX_BYTES + (kk & 3) * 32) >> 4), id_qk, kk > 0 ? 1u : 0u);
           // q^PE x k^PE tileᵀ (last box), 4 k-steps of 16; PAIR: each rank takes two of them, so the
           // partial logits carry half of the RoPE term each and the two QKs take equal time
 #pragma unroll
           for (int kk = (C::PAIR ? 2 * int(crank) : 0); kk < (C::PAIR ? 2 * int(crank) + 2 : 4); ++kk)
-            mma_ss(s_tmem, qpe_desc + uint64_t(kk * 2),
-                   kv_desc + uint64_t(((C::NBOX - 1) * C::BOX_BYTES + kk * 32) >> 4), id_qk, 1u);
+            if (!(MODE & 32))
+              mma_ss(s_tmem, qpe_desc + uint64_t(kk * 2),
+                     kv_desc + uint64_t(((C::NBOX - 1) * C::BOX_BYTES + kk * 32) >> 4), id_qk, 1u);
           mma_commit(&s_full[g % C::NSB]);
           TRACE(4, g);
         }
@@ -514,7 +532,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         if (q4 == 0 && lane == 0) TRACE(18, g);
         mbar_wait(&s_full[sb], (g / C::NSB) & 1);
         if (q4 == 0 && lane == 0) TRACE(2, g);
-        if (!q_active) {                                 // no head rows here: P stays 0 (S rows are 0)
+        if (!q_active || (MODE & 16)) {                  // no head rows here: P stays 0 (S rows are 0)
           if (lane == 0) mbar_arrive(&p_full[sb]);
           continue;
         }
@@ -926,6 +944,8 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
   if (mode && strcmp(mode, "stream") == 0) return launch_tc_mode<W_LAT, 1>(map, a, n_cta, s);
   if (mode && strcmp(mode, "nold") == 0) return launch_tc_mode<W_LAT, 8>(map, a, n_cta, s);
   if (mode && strcmp(mode, "notma") == 0) return launch_tc_mode<W_LAT, 4>(map, a, n_cta, s);
+  if (mode && strcmp(mode, "nosm") == 0) return launch_tc_mode<W_LAT, 4 | 16>(map, a, n_cta, s);
+  if (mode && strcmp(mode, "nomma") == 0) return launch_tc_mode<W_LAT, 4 | 32>(map, a, n_cta, s);
   if (mode && strncmp(mode, "trace", 5) == 0) {   // trace, trace_notma, trace_nold
     static long long* buf = nullptr;
     const int nb = kSlots * kTrace + 2 * n_cta;
@@ -934,7 +954,8 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
     b.trace = buf;
     const char* tc = getenv("TPLA_K3_TRACE_CTA");
     b.trace_cta = tc ? atoi(tc) : 0;
-    cudaError_t e = strcmp(mode, "trace_notma") == 0 ? launch_tc_mode<W_LAT, 6>(map, b, n_cta, s)
+    cudaError_t e = strcmp(mode, "trace_notma") == 0   ? launch_tc_mode<W_LAT, 6>(map, b, n_cta, s)
+                    : strcmp(mode, "trace_nosm") == 0  ? launch_tc_mode<W_LAT, 2 | 4 | 16>(map, b, n_cta, s)
                     : strcmp(mode, "trace_nold") == 0  ? launch_tc_mode<W_LAT, 10>(map, b, n_cta, s)
                                                         : launch_tc_mode<W_LAT, 2>(map, b, n_cta, s);
     static long long h[kSlots * kTrace + 4 * kMaxCta + 16];
@@ -968,8 +989,14 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
     for (int g = 0; g < kTrace; ++g)
       fprintf(stderr, "[k3 trace] %3d %8lld %8lld %8lld %8lld %8lld %8lld\n", g, h[g] - h[0], h[4 * kTrace + g] - h[0],
               h[2 * kTrace + g] - h[0], h[3 * kTrace + g] - h[0], h[kTrace + g] - h[0], h[5 * kTrace + g] - h[0]);
-    fprintf(stderr, "[k3 tma] g tma_issue qk_issue (rel. to qk_issue[0])\n");
-    for (int g = 0; g < kTrace; ++g) fprintf(stderr, "[k3 tma] %3d %8lld %8lld\n", g, h[14 * kTrace + g] - h[0], h[g] - h[0]);
+    fprintf(stderr, "[k3 tma] g tma_issue landed qk_issue (rel. to qk_issue[0])\n");
+    for (int g = 0; g < kTrace; ++g)
+      fprintf(stderr, "[k3 tma] %3d %8lld %8lld %8lld\n", g, h[14 * kTrace + g] - h[0], h[22 * kTrace + g] - h[0],
+              h[g] - h[0]);
+    fprintf(stderr, "[k3 mma] g kv_wait_start kv_wait_done qk_issue pv_wait_start(g) pv_issue(g) (rel. qk_issue[0])\n");
+    for (int g = 0; g < kTrace; ++g)
+      fprintf(stderr, "[k3 mma] %3d %8lld %8lld %8lld %8lld %8lld\n", g, h[19 * kTrace + g] - h[0],
+              h[20 * kTrace + g] - h[0], h[g] - h[0], h[21 * kTrace + g] - h[0], h[kTrace + g] - h[0]);
     fprintf(stderr, "[k3 xchg] g x_ok sent x_full (warp 4, rel. to s_ready)\n");
     for (int g = 0; g < kTrace; ++g)
       fprintf(stderr, "[k3 xchg] %3d %6lld %6lld %6lld\n", g, h[19 * kTrace + g] - h[2 * kTrace + g],
