@@ -174,8 +174,8 @@ tpla_status tpla_append_kv(const tpla_config* cfg, const tpla_weights* w, const 
                            int32_t n, int32_t rms_mode, int32_t* n_dropped, void* stream);
 
 /* PD-separated prefill: the prompt rows are written to this device's
- * cache with the EXACT (unsliced) RMS, so decode reuses the MLA prefill cache.  The causal MLA
- * prefill attention itself is not part of this build (returns TPLA_ERR_UNSUPPORTED if q != NULL). */
+ * cache with the EXACT (unsliced) RMS, so decode reuses the MLA prefill cache.  q must be NULL:
+ * the causal prefill attention is tpla_prefill_attention (returns TPLA_ERR_UNSUPPORTED otherwise). */
 tpla_status tpla_prefill_mla(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
                              const void* c_kv, const void* k_pe, const int32_t* seq_idx, const int32_t* pos,
                              int32_t n, const void* q, void* stream);
@@ -211,6 +211,23 @@ tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpl
  *   ws: tpla_decode_workspace_bytes_mtp(cfg, B, n_q, max_seq_len) bytes.  tpla_decode = n_q 1. */
 tpla_status tpla_decode_workspace_bytes_mtp(const tpla_config* cfg, int32_t B, int32_t n_q, int32_t max_seq_len,
                                             size_t* bytes);
+
+/* Causal prefill attention of one prompt.  The prompt's
+ * L rows must already be in this device's cache as sequence `seq`, positions 0..L-1 (written by
+ * tpla_prefill_mla: EXACT rows).  Every prompt token t attends to rows 0..t with this
+ * device's shard softmax (g = 1: plain MLA with the heads split over k devices — the PD-separated
+ * prefill; g > 1: TPLA prefill over the latent shard, the paper's comparison), then W^UV, W^O and the
+ * all-reduce over comm exactly as tpla_decode.
+ * Computed as the multi-token decode (tpla_decode_mtp) over pseudo-sequences that share the
+ * prompt's pages: pseudo-sequence j holds n_q = 128 / H_loc consecutive prompt tokens as its newest
+ * tokens, with causal per-row limits; chunks of <= 256 prompt rows per decode call.
+ *   q_nope [L, h_q, d_h], q_pe [L, h_q, d_r] bf16 (device, post-RoPE); y [L, D] fp32 (= or +=
+ *   with TPLA_DECODE_ACCUMULATE), out [L, D] bf16 or NULL; ws: tpla_prefill_workspace_bytes.
+ *   Needs the tcgen05 attention path (d_r = 64, W_lat in {64, 128, 256, 512}).  Errors as tpla_decode. */
+tpla_status tpla_prefill_workspace_bytes(const tpla_config* cfg, int32_t L, int32_t max_pages_per_seq, size_t* bytes);
+tpla_status tpla_prefill_attention(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                                   const void* q_nope, const void* q_pe, int32_t seq, int32_t L, void* ws,
+                                   size_t ws_bytes, float* y, void* out, int32_t flags, tpla_comm* comm, void* stream);
 
 /* Up-projection shared by a latent group.  The g devices j of head block i hold
  * the same W^O rows, so Õ_i = Σ_j v_j W^O_i = (Σ_j v_j) W^O_i: the group may sum its

@@ -80,6 +80,9 @@ _SIGS = {
     "tpla_decode": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _P, _I, _I, _P,
                      _S, _P, _P, _I, _P, _P], _I),
     "tpla_decode_workspace_bytes_mtp": ([C.POINTER(tpla_config), _I, _I, _I, C.POINTER(_S)], _I),
+    "tpla_prefill_workspace_bytes": ([C.POINTER(tpla_config), _I, _I, C.POINTER(_S)], _I),
+    "tpla_prefill_attention": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _I, _I,
+                                _P, _S, _P, _P, _I, _P, _P], _I),
     "tpla_decode_v": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _P, _I, _I, _I,
                        _P, _S, _P, _I, _I, _P], _I),
     "tpla_project_out": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), _P, _I, _I, _I, _P, _S, _P, _P, _I, _P,
@@ -212,6 +215,20 @@ def tpla_decode_mtp(cfg, w, cache, q_nope, q_pe, seq_lens, B, n_q, max_seq_len, 
     _check(_lib.tpla_decode_mtp(C.byref(cfg), C.byref(w), C.byref(cache), _ptr(q_nope), _ptr(q_pe), _ptr(seq_lens), B,
                                 n_q, max_seq_len, _ptr(ws), ws_bytes, _ptr(y), _ptr(out), flags, comm, _ptr(stream)),
            "tpla_decode_mtp")
+
+
+def tpla_prefill_workspace_bytes(cfg, L, max_pages_per_seq):
+    n = _S(0)
+    _check(_lib.tpla_prefill_workspace_bytes(C.byref(cfg), L, max_pages_per_seq, C.byref(n)),
+           "tpla_prefill_workspace_bytes")
+    return n.value
+
+
+def tpla_prefill_attention(cfg, w, cache, q_nope, q_pe, seq, L, ws, ws_bytes, y, out=None, flags=0, comm=None,
+                           stream=0):
+    _check(_lib.tpla_prefill_attention(C.byref(cfg), C.byref(w), C.byref(cache), _ptr(q_nope), _ptr(q_pe), seq, L,
+                                       _ptr(ws), ws_bytes, _ptr(y), _ptr(out), flags, comm, _ptr(stream)),
+           "tpla_prefill_attention")
 
 
 def tpla_decode_v(cfg, w, cache, q_nope, q_pe, seq_lens, B, n_q, max_seq_len, ws, ws_bytes, v_acc, n_chunks=1, flags=0,

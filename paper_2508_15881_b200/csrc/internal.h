@@ -111,6 +111,10 @@ size_t wo_tc_part_bytes(int N, int K, int B);
 cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, void* part_ws, float* y,
                          bool accumulate, uint16_t* out_bf16, cudaStream_t s, int k_begin = 0, int k_len = 0);
 
+// K6: page-table rows + lengths of the prefill pseudo-sequences (k6_prefill.cu)
+cudaError_t launch_prefix_table(const int32_t* block_table, int seq, int max_pages, int n_full, int n_q, int r0,
+                                int n_rows, int32_t* table, int32_t* lens, cudaStream_t s);
+
 // y[b, n] (=|+=) sum_ks y_part[ks, b, n]
 cudaError_t launch_reduce_slices(const float* y_part, int kslices, int B, int N, float* y, bool accumulate,
                                  cudaStream_t s);

@@ -588,6 +588,89 @@ tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const
   return ok();
 }
 
+// ---- prefill attention as multi-token decode over prefixes (k6_prefill.cu) ----
+namespace {
+struct PrefillPlan {
+  int n_q;        // prompt tokens per pseudo-sequence: n_q * H_loc <= 128 MMA rows
+  int rows;       // prompt rows per chunk (one decode call; <= 256 keeps the tcgen05 W^O path)
+  int n_chunks;
+  size_t dec_bytes, tab_bytes, total;
+};
+PrefillPlan prefill_plan(const Geom& g, int L, int max_pages) {
+  PrefillPlan p{};
+  p.n_q = std::max(1, 128 / g.h_loc);
+  p.rows = std::max(p.n_q, (256 / p.n_q) * p.n_q);
+  p.n_chunks = (L + p.rows - 1) / p.rows;
+  const int n_seq = p.rows / p.n_q + 1;                     // (+1: the remainder pseudo-sequence)
+  // the two decode calls of a chunk: rows / n_q pseudo-sequences of n_q tokens, and one of the
+  // remainder (ws_layout is not monotonic in the row count: <= 256 rows add the tcgen05 W^O partials)
+  p.dec_bytes = align256(std::max(ws_layout(g, p.rows / p.n_q, p.n_q, L).total,
+                                  ws_layout(g, 1, std::max(1, p.n_q - 1), L).total));
+  p.tab_bytes = align256(size_t(n_seq) * (max_pages + 1) * 4);
+  p.total = p.dec_bytes + size_t(p.n_chunks) * p.tab_bytes;
+  return p;
+}
+}  // namespace
+
+tpla_status tpla_prefill_workspace_bytes(const tpla_config* cfg, int32_t L, int32_t max_pages_per_seq, size_t* bytes) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return st;
+  if (!bytes || L < 1 || max_pages_per_seq < 1) return fail(TPLA_ERR_INVALID_ARG, "L=%d, max_pages=%d", L, max_pages_per_seq);
+  *bytes = prefill_plan(g, L, max_pages_per_seq).total;
+  return ok();
+}
+
+tpla_status tpla_prefill_attention(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                                   const void* q_nope, const void* q_pe, int32_t seq, int32_t L, void* ws,
+                                   size_t ws_bytes, float* y, void* out, int32_t flags, tpla_comm* comm,
+                                   void* stream) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return st;
+  if (!cache || !cache->block_table) return fail(TPLA_ERR_INVALID_ARG, "NULL cache");
+  if (seq < 0 || seq >= cache->batch) return fail(TPLA_ERR_SHAPE, "seq=%d outside [0, %d)", seq, cache->batch);
+  if (L < 1 || int64_t(L) > int64_t(cache->max_pages_per_seq) * cache->page_size)
+    return fail(TPLA_ERR_CAPACITY, "L=%d outside the page table", L);
+  if (!q_nope || !q_pe || !y || !ws) return fail(TPLA_ERR_INVALID_ARG, "NULL q_nope/q_pe/y/ws");
+  const PrefillPlan p = prefill_plan(g, L, cache->max_pages_per_seq);
+  if (!(use_tc_attention(g, p.rows / p.n_q + 1) && combine_wuv_supported(g)))
+    return fail(TPLA_ERR_UNSUPPORTED, "prefill attention needs the tcgen05 path (W_lat=%d, d_r=%d)", g.w_lat, g.d_r);
+  if (ws_bytes < p.total) return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, p.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(ws);
+  const auto* qn = static_cast<const uint16_t*>(q_nope);
+  const auto* qp = static_cast<const uint16_t*>(q_pe);
+  auto* o16 = static_cast<uint16_t*>(out);
+  const int n_seq_max = p.rows / p.n_q + 1;
+  for (int c = 0; c < p.n_chunks; ++c) {
+    const int r0 = c * p.rows, nr = std::min(p.rows, L - r0);
+    const int full = nr / p.n_q, rem = nr % p.n_q;
+    // each chunk has its own table region: a later chunk's table kernel may start (PDL) while
+    // this chunk's attention still reads its table
+    auto* table = reinterpret_cast<int32_t*>(base + p.dec_bytes + size_t(c) * p.tab_bytes);
+    int32_t* lens = table + size_t(n_seq_max) * cache->max_pages_per_seq;
+    cudaError_t e = launch_prefix_table(cache->block_table, seq, cache->max_pages_per_seq, full, p.n_q, r0, nr, table,
+                                        lens, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K6 prefix table");
+    tpla_cache pc = *cache;
+    pc.block_table = table;
+    struct Part { int n_seq, n_q, row0; };
+    const Part parts[2] = {{full, p.n_q, r0}, {rem ? 1 : 0, rem, r0 + full * p.n_q}};
+    for (int k = 0; k < 2; ++k) {
+      if (parts[k].n_seq == 0) continue;
+      pc.batch = parts[k].n_seq;
+      pc.block_table = table + size_t(k ? full : 0) * cache->max_pages_per_seq;
+      const size_t r = size_t(parts[k].row0);
+      st = tpla_decode_mtp(cfg, w, &pc, qn + r * g.h_q * g.d_h, qp + r * g.h_q * g.d_r, lens + (k ? full : 0),
+                           parts[k].n_seq, parts[k].n_q, L, base, p.dec_bytes, y + r * g.D, o16 ? o16 + r * g.D : nullptr,
+                           flags, comm, stream);
+      if (st) return st;
+    }
+  }
+  return ok();
+}
+
 tpla_status tpla_decode_v(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache, const void* q_nope,
                           const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t n_q, int32_t max_seq_len,
                           void* ws, size_t ws_bytes, float* v_acc, int32_t n_chunks, int32_t flags, void* stream) {

@@ -153,6 +153,18 @@ class TplaRank:
         abi.tpla_prefill_mla(self.cfg, self.weights, self.cache, c_kv, k_pe, seq_idx, pos, n, None,
                              stream_ptr(stream))
 
+    # ---- prefill attention: the prompt's rows must be in the cache (prefill())
+    def prefill_attention(self, q_nope, q_pe, seq: int, y, out=None, *, accumulate=False, comm=None, stream=None):
+        """q_nope [L, h_q, d_h], q_pe [L, h_q, d_r]; y/out [L, D]: causal attention of the prompt held as
+        cache sequence `seq` (positions 0..L-1), then W^UV, W^O (+ all-reduce)."""
+        L = int(q_nope.shape[0])
+        need = abi.tpla_prefill_workspace_bytes(self.cfg, L, self.max_pages)
+        if getattr(self, "pf_ws", None) is None or self.pf_ws.numel() < need:
+            self.pf_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        abi.tpla_prefill_attention(self.cfg, self.weights, self.cache, q_nope, q_pe, seq, L, self.pf_ws,
+                                   self.pf_ws.numel(), y, out, abi.DECODE_ACCUMULATE if accumulate else 0, comm,
+                                   stream_ptr(stream))
+
     # ---- K2..K5 (+ C1)
     def decode(self, q_nope, q_pe, seq_lens, y, out=None, *, B: int | None = None, accumulate=False, comm=None,
                stream=None):

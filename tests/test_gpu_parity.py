@@ -554,3 +554,54 @@ def test_full_size_sampled_attention_c1():
         Oref, _, _, _ = tpla.shard_attention(f64(bits_from_bf16(q_lat[b])), f64(bits_from_bf16(qpe[b])), rows,
                                               pl.w_lat, dims_scale(dims))
         assert row_rel_err(O[b].cpu().numpy(), Oref) <= TOL
+
+
+# ----------------------------------------------------------------------------- prefill (f1)
+def prefill_case(d, dims, k, g, kind, L, *, sample=None, seed=0):
+    """causal prefill attention of one prompt (cache sequence 1), every rank of a (k, g)
+    plan on this GPU accumulating y.  Pinned to the oracle's decode step over each prefix: prompt
+    token t attends to rows 0..t (P:137-141 per token; g = 1 is plain MLA)."""
+    xf, sseed, U, U32, alpha = transform_inputs(kind, dims, 41, g)
+    basis = U if kind == "pca" else None
+    w = synth.gen_weights(dims, seed + 1)
+    q, qpe = synth.gen_queries(dims, L, seed + 2)                # row t = prompt token t
+    c_raw = synth.gen_raw_ckv(dims, L, seed + 3, 1, basis=basis)
+    k_pe = synth.gen_kpe(dims, L, seed + 3, 1)
+    junk = synth.gen_raw_ckv(dims, 64, seed + 4, 0, basis=basis)   # sequence 0: another prompt
+    y = torch.zeros((L, dims.D), dtype=torch.float32, device=d)
+    out = torch.empty((L, dims.D), dtype=torch.bfloat16, device=d)
+    for rid in range(k):
+        r = TplaRank(spec_of(dims), k=k, g=g, rank=rid, batch=2, max_seq_len=L + 64, device=d, page_perm_seed=rid + 5)
+        r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=xf, sign_seed=sseed, U_pca=U32, alpha=alpha)
+        r.prefill(bf16_from_bits(junk, d), bf16_from_bits(synth.gen_kpe(dims, 64, seed + 4, 0), d),
+                  torch.zeros(64, dtype=torch.int32, device=d), torch.arange(64, dtype=torch.int32, device=d))
+        r.prefill(bf16_from_bits(c_raw, d), bf16_from_bits(k_pe, d), torch.ones(L, dtype=torch.int32, device=d),
+                  torch.arange(L, dtype=torch.int32, device=d))
+        r.prefill_attention(bf16_from_bits(q, d), bf16_from_bits(qpe, d), 1, y, out if rid == k - 1 else None,
+                            accumulate=rid > 0)
+    torch.cuda.synchronize()
+    got = y.cpu().numpy()
+    ts = range(L) if sample is None else sorted(set(list(range(0, L, sample)) + [L - 1, L - 2]))
+    for t in ts:
+        pb = tpla.Problem(W_UK=f64(w.W_UK), W_UV=f64(w.W_UV), gamma=f64(w.gamma), W_O=f64(w.W_O), U=U,
+                          alpha=np.asarray(alpha, float), mu=np.asarray(alpha, float),
+                          c_raw=[f64(c_raw[:t + 1])], k_pe=[f64(k_pe[:t + 1])], modes=[[tpla.EXACT] * (t + 1)],
+                          q_nope=f64(q[t:t + 1]), q_pe=f64(qpe[t:t + 1]), h_q=dims.h_q, d_h=dims.d_h, eps=1e-6,
+                          sm_scale=dims_scale(dims))
+        ref = tpla.tpla_decode_step(pb, k, g, round_rows=numerics.round_bf16)
+        e = row_rel_err(got[t:t + 1], ref)
+        assert e <= TOL, (t, e)
+    assert torch.equal(out, y.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("dname,k,g,kind,L", [("dsv3", 2, 1, "identity", 71), ("dsv3", 1, 1, "hadamard", 40),
+                                              ("kimi", 4, 2, "hadamard", 45), ("dsv3", 2, 2, "hadamard", 66)])
+def test_prefill_attention(dname, k, g, kind, L):
+    """g = 1: the PD-separated MLA prefill (heads split over k); g > 1: TPLA prefill.  Ragged
+    n_q remainders (L % n_q != 0)."""
+    prefill_case(dev(), synth.PRESETS[dname], k, g, kind, L)
+
+
+def test_prefill_attention_chunks():
+    """More prompt rows than one decode call takes (256): two chunks plus a remainder, sampled."""
+    prefill_case(dev(), synth.PRESETS["dsv3"], 2, 1, "hadamard", 517, sample=23)
