@@ -118,6 +118,14 @@ struct Cfg {
   // tile g (with two buffers the softmax waited ~470 cycles per tile for it, measured).
   static constexpr int NSB = W_LAT == 64 ? 3 : 2;
   static constexpr int LAG = NSB - 1;                 // PV issued LAG tiles behind QK
+  // SPLIT: QK and PV issued by two warps (w1, w2) with their own loops.  Measured A/B: W_lat = 64
+  // (h8, c3) 1.5-2 % faster; W_lat = 256 (c1) 5 % slower (its PV / QK waits interleave better in
+  // one loop); W_lat = 128 neutral.  Not for the CTA pair.
+#ifdef TPLA_K3_NO_SPLIT
+  static constexpr bool SPLIT = false;
+#else
+  static constexpr bool SPLIT = !PAIR && W_LAT == 64;
+#endif
   static constexpr int SUB = TT / kSub;               // TMA boxes per column group per tile
   static constexpr int CH = TT / 2;                   // S columns per softmax warp
   static constexpr int SEQ_COST = 512 / TT;           // per-sequence header cost in tiles (schedule)
@@ -352,6 +360,81 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         }
         if (lane == 0) TRACE(22, g);
       }
+  } else if (C::SPLIT && (warp == 1 || warp == 2)) {
+    // ============================================================ MMA issuers, split: w1 QK, w2 PV
+    // One issuing warp spent ~1340 cycles per 128-token tile on its waits, elects and descriptor
+    // setup (trace, W_lat = 64) for 768 cycles of tensor work.  Two independent loops halve the
+    // steps each warp takes per tile; their ordering constraints become mbarrier waits:
+    //   QK(g) needs its tile (kv_full), its segment's Q' (q_ready) and S buffer g % NSB free: the
+    //         PV of tile g - NSB complete (pv_done, committed by the PV warp);
+    //   PV(g) needs P(g) (p_full; implies QK(g) complete, and for a segment's first PV that the
+    //         previous segment's epilogue has read O).  Its commits release the ring stage
+    //         (both MMAs of the tile have read it) and signal pv_done.
+    // (tcgen05.commit tracks the issuing thread's own MMAs: each warp commits what it issued.)
+    constexpr uint32_t id_qk = idesc_bf16(128, C::TT, false, false);
+    constexpr uint32_t id_pv = idesc_bf16(128, C::WL, false, true);
+    constexpr uint32_t hi_k = desc_sw128_hi(1024);           // K-major: SBO = 1024 B (8-row groups)
+    const uint32_t kv0 = smem_addr(s_kv);
+    int g = 0, seg = 0;
+    if (warp == 1) {
+      const uint64_t qpe_desc = make_desc(smem_addr(s_qpe), 16, hi_k);
+      for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
+        const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
+        mbar_wait(&q_ready, seg & 1);
+        if (seg == 0 && lane == 0) EV(6);
+        for (int t = t0; t < t1; ++t, ++g) {
+          const int st = g % C::NST, sb = g % C::NSB;
+          if (lane == 0) TRACE(19, g);
+          mbar_wait(&kv_full[st], (g / C::NST) & 1);
+          if (g >= C::NSB) mbar_wait(&pv_done[sb], ((g / C::NSB) & 1) ^ 1);   // PV(g - NSB) complete
+          if (lane == 0) TRACE(20, g);
+          if (g == 0 && lane == 0) EV(7);
+          tc_fence_after();
+          if (elect_one()) {
+            TRACE(0, g);
+            const uint64_t kv_desc = make_desc(kv0 + st * C::STAGE_BYTES, 16, hi_k);
+            const uint32_t s_tmem = tb + C::S_COL0 + sb * C::TT;
+#pragma unroll
+            for (int kk = 0; kk < C::WL / 16; ++kk)
+              if (!(MODE & 32))
+                mma_ts(s_tmem, tb + C::Q_COL + kk * 8,
+                       kv_desc + uint64_t(((kk >> 2) * C::BOX_BYTES + (kk & 3) * 32) >> 4), id_qk, kk > 0 ? 1u : 0u);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              if (!(MODE & 32))
+                mma_ss(s_tmem, qpe_desc + uint64_t(kk * 2),
+                       kv_desc + uint64_t(((C::NBOX - 1) * C::BOX_BYTES + kk * 32) >> 4), id_qk, 1u);
+            mma_commit(&s_full[sb]);
+            TRACE(4, g);
+          }
+          __syncwarp();
+        }
+      }
+    } else {
+      for (int b = S.b_first; b <= S.b_last; ++b) {
+        const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
+        for (int t = t0; t < t1; ++t, ++g) {
+          const int st = g % C::NST, sb = g % C::NSB;
+          if (lane == 0) TRACE(21, g);
+          mbar_wait(&p_full[sb], (g / C::NSB) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            TRACE(1, g);
+            const uint64_t v_desc = make_desc(kv0 + st * C::STAGE_BYTES, C::BOX_BYTES, hi_k);
+            const uint32_t p_tmem = tb + C::S_COL0 + sb * C::TT;
+#pragma unroll
+            for (int kk = 0; kk < C::TT / 16; ++kk)
+              if (!(MODE & 32))
+                mma_ts(tb + C::O_COL, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), id_pv,
+                       (t == t0 && kk == 0) ? 0u : 1u);
+            mma_commit(&kv_empty[st]);
+            mma_commit(&pv_done[sb]);
+            TRACE(5, g);
+          }
+          __syncwarp();
+        }
+      }
+    }
   } else if (warp == 1) {
     // ============================================================ MMA issuer (converged warp, one issuer)
     constexpr uint32_t id_qk = idesc_bf16(128, C::TT, false, false);
