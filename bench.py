@@ -48,6 +48,11 @@ WORKLOADS = {
     # SURVEY §8(d) headline shape: one latent shard per GPU on 8 GPUs (all k=8 shards on one GPU here)
     "h8": dict(desc="SURVEY 8(d) headline shape: DeepSeek-V3 32K context, batch 32, g=8 (one latent shard per GPU "
                     "at 8 GPUs)", model="dsv3", B=32, S=32768, g=8, xform="hadamard"),
+    # the same 8-GPU 32K shape with the paper's TP > 2 recipe: g = 2 latent shards, heads
+    # split 4 ways (H_loc = 32, W = 320): all k = 8 ranks on one GPU
+    "h8g2": dict(desc="SURVEY 8(d) headline, paper's TP>2 recipe: DeepSeek-V3 32K context, batch 32, g=2 with heads "
+                      "split over k=8 (H_loc=32; the 8-GPU per-GPU shard)", model="dsv3", B=32, S=32768, g=2, k=8,
+                 xform="hadamard"),
     # configs[4] baseline: replicated-MLA cache (g = 1); "mla2" = the paper's MLA TP=2 (heads split)
     "mla1": dict(desc="configs[4] baseline: MLA (g=1, replicated 576-wide cache), DeepSeek-V3 32K, batch 32, "
                       "all heads on one rank", model="dsv3", B=32, S=32768, g=1, xform="identity"),
