@@ -530,14 +530,16 @@ def test_decode_v_project_out_nccl_world1_equals_decode():
     assert torch.equal(out, y1.to(torch.bfloat16))
 
 
-def test_full_size_sampled_attention_c1():
-    """configs[1] shard at full size (B=32, S=32K, H_loc=128, W=320) in the bench's launch
-    configuration; two sampled sequences checked against the oracle."""
+@pytest.mark.parametrize("k,g,B,S", [(2, 2, 32, 32768), (8, 8, 32, 32768), (8, 2, 32, 32768), (8, 8, 16, 131072)])
+def test_full_size_sampled_attention_c1(k, g, B, S):
+    """Full-size shards in the bench's launch configuration: configs[1] (c1: H_loc=128, W=320),
+    the 8-GPU 32K shape at g = 8 (h8: W_lat = 64, ping-pong softmax, split issuers) and with the
+    paper's TP > 2 recipe (h8g2: H_loc = 32), configs[3] (c3: 128K); two sampled sequences checked
+    against the oracle."""
     d = dev()
     dims = synth.PRESETS["dsv3"]
-    g, B, S = 2, 32, 32768
-    r = TplaRank(spec_of(dims), k=2, g=2, rank=1, batch=B, max_seq_len=S, device=d)
-    pl = oplan.make_plan(2, 2, dims.h_q, dims.d_c, dims.d_r, 1)
+    r = TplaRank(spec_of(dims), k=k, g=g, rank=k - 1, batch=B, max_seq_len=S, device=d)
+    pl = oplan.make_plan(k, g, dims.h_q, dims.d_c, dims.d_r, k - 1)
     gen = torch.Generator(device=d)
     gen.manual_seed(123)
     r.cache_buf[..., :pl.row_width].normal_(generator=gen)
@@ -548,10 +550,11 @@ def test_full_size_sampled_attention_c1():
     O = torch.zeros((B, pl.h_loc, pl.w_lat), dtype=torch.float32, device=d)
     r.decode_attention(q_lat, qpe, lens, O)
     torch.cuda.synchronize()
-    for b in (5, 31):
+    for b in (5, B - 1):
         n = int(lens[b])
         rows = f64(r.cache_rows_bits(b, n)[:, :pl.row_width])
-        Oref, _, _, _ = tpla.shard_attention(f64(bits_from_bf16(q_lat[b])), f64(bits_from_bf16(qpe[b])), rows,
+        Oref, _, _, _ = tpla.shard_attention(f64(bits_from_bf16(q_lat[b])),
+                                              f64(bits_from_bf16(qpe[b, pl.head_begin:pl.head_end])), rows,
                                               pl.w_lat, dims_scale(dims))
         assert row_rel_err(O[b].cpu().numpy(), Oref) <= TOL
 
