@@ -608,3 +608,10 @@ def test_prefill_attention(dname, k, g, kind, L):
 def test_prefill_attention_chunks():
     """More prompt rows than one decode call takes (256): two chunks plus a remainder, sampled."""
     prefill_case(dev(), synth.PRESETS["dsv3"], 2, 1, "hadamard", 517, sample=23)
+
+
+def test_e2e_parity_ragged_combine_blocks():
+    """B = 33 sequences: three 16-row K45 blocks per head, the last one ragged."""
+    S_list = [1 + (7 * b) % 97 for b in range(33)]
+    e2e_case(dev(), synth.PRESETS["dsv3"], 2, 2, "hadamard", S_list)
+    e2e_case(dev(), synth.PRESETS["dsv3"], 2, 2, "hadamard", S_list, wo="shared")
