@@ -128,13 +128,49 @@ def test_decode_rejects_before_launch():
     assert abi.tpla_launch_count() == n_before
 
 
-def test_prefill_attention_is_declared_unsupported():
+def test_prefill_mla_with_q_points_to_prefill_attention():
     c = cfg()
     w = abi.tpla_weights(None, None, None, None, 0, 2.0, 2.0)
     cache = abi.tpla_cache(1 << 20, 1 << 20, 16, 64, 4, 320, 2)
     with pytest.raises(abi.TplaError) as ei:
         abi.tpla_prefill_mla(c, w, cache, 1 << 20, 1 << 20, 1 << 20, 1 << 20, 4, 1 << 20)
     assert ei.value.status == abi.ERR_UNSUPPORTED
+
+
+def test_prefill_attention_host_checks():
+    """Workspace sizing (host only) and validation before any launch."""
+    c = cfg()
+    a = abi.tpla_prefill_workspace_bytes(c, 256, 8)
+    b = abi.tpla_prefill_workspace_bytes(c, 1024, 16)      # four chunks of 256 prompt rows
+    assert 0 < a < b
+    with pytest.raises(abi.TplaError):
+        abi.tpla_prefill_workspace_bytes(c, 0, 8)
+    w = abi.tpla_weights(1 << 20, 1 << 20, 1 << 20, None, 0, 2.0, 2.0)
+    cache = abi.tpla_cache(1 << 20, 1 << 20, 16, 64, 4, 320, 2)
+    n_before = abi.tpla_launch_count()
+    with pytest.raises(abi.TplaError) as ei:              # prompt longer than the page table
+        abi.tpla_prefill_attention(c, w, cache, 1 << 20, 1 << 20, 0, 300, 1 << 20, 1 << 30, 1 << 20)
+    assert ei.value.status == abi.ERR_CAPACITY
+    with pytest.raises(abi.TplaError) as ei:              # sequence index outside the cache
+        abi.tpla_prefill_attention(c, w, cache, 1 << 20, 1 << 20, 2, 64, 1 << 20, 1 << 30, 1 << 20)
+    assert ei.value.status == abi.ERR_SHAPE
+    with pytest.raises(abi.TplaError) as ei:
+        abi.tpla_prefill_attention(c, w, cache, None, 1 << 20, 0, 64, 1 << 20, 1 << 30, 1 << 20)
+    assert ei.value.status == abi.ERR_INVALID_ARG
+    assert abi.tpla_launch_count() == n_before
+
+
+def test_project_out_host_checks():
+    """Group-shared up-projection: chunking rules checked before any launch."""
+    c = cfg()
+    w = abi.tpla_weights(1 << 20, 1 << 20, 1 << 20, None, 0, 2.0, 2.0)
+    n_before = abi.tpla_launch_count()
+    for n_chunks, chunk, status in [(3, 0, abi.ERR_DIVISIBILITY), (2, 2, abi.ERR_INVALID_ARG),
+                                    (0, 0, abi.ERR_INVALID_ARG)]:
+        with pytest.raises(abi.TplaError) as ei:
+            abi.tpla_project_out(c, w, 1 << 20, 4, n_chunks, chunk, 1 << 20, 1 << 30, 1 << 20)
+        assert ei.value.status == status
+    assert abi.tpla_launch_count() == n_before
 
 
 def test_import_fails_loudly_without_library(tmp_path):
