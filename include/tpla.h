@@ -194,7 +194,12 @@ tpla_status tpla_decode_workspace_bytes(const tpla_config* cfg, int32_t B, int32
  *   is all-reduced in place (sum over the k devices);  out: device bf16 [B, D] or NULL:
  *   bf16(y) after the all-reduce.  A process may hold m of the k ranks: it calls tpla_decode once
  *   per held rank with TPLA_DECODE_ACCUMULATE after the first and passes comm (world = k/m
- *   processes) only on the last call, so the all-reduce sums every rank exactly once. */
+ *   processes) only on the last call, so the all-reduce sums every rank exactly once.
+ *   Ordering: the kernels use programmatic dependent launch; K3 reads seq_lens and the block table
+ *   BEFORE waiting for its predecessor kernels (its schedule overlaps their tail), so the caller's
+ *   writes to those two arrays must be complete when the call is enqueued (a copy, or a kernel
+ *   that does not trigger its dependents early).  Every other input may come from the preceding
+ *   kernels of the stream (e.g. tpla_append_kv of the same step). */
 tpla_status tpla_decode(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
                         const void* q_nope, const void* q_pe, const int32_t* seq_lens, int32_t B,
                         int32_t max_seq_len, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,

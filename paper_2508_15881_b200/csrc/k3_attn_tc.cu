@@ -230,7 +230,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   if (C::PAIR) cluster_sync();   // the peer's barriers are initialised before any remote operation
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
   if (tid == 0) s_before = 0;
-  pdl_wait();   // everything below reads the predecessors' outputs (seq_lens, Q', cache rows)
+  // The schedule and the page-table lookups read only caller inputs (seq_lens, the block table:
+  // their writes must be complete before tpla_decode is called, tpla.h), so they run before the
+  // PDL wait, overlapping the predecessor's tail; the wait comes right before the first read of a
+  // predecessor's output — the producer's first TMA (the cache rows K1 appended) and the softmax
+  // warps' first Q' load (K2) — and before any write (the epilogue's partials, read by the
+  // previous step's K45).  The MMA warps only consume what those threads hand over.
   if (threadIdx.x == 0) EV(1);
   if (warp == 3) {
     // tiles per sequence -> exclusive prefix sum (warp scan, 32 sequences per step)
@@ -307,6 +312,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     if (lane == 0) EV(2);
     int rows_cur = lookup(lane), rows_next = lookup(32 + lane);
     if (__shfl_sync(0xffffffffu, rows_cur + rows_next, 0) >= 0 && lane == 0) EV(3);
+    pdl_wait();
     for (int t = S.lo, g = 0; t < S.hi; ++t, ++g) {
       const int u0 = g * C::SUB;                       // SUB divides 32: a tile never spans batches
       if (u0 > 0 && (u0 & 31) == 0) {
@@ -345,6 +351,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         __syncwarp();
       }
   } else if (MODE == 1) {
+    pdl_wait();
     if (warp == 4 && lane == 0) {   // keep K4's segment map valid (values are meaningless)
       int seg = 0;
       for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
@@ -603,6 +610,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       return (a0 + a1) + (a2 + a3);
     };
     int g = 0, seg = 0;
+    pdl_wait();
     if (S.b_first <= S.b_last) load_q(S.b_first);
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
@@ -734,6 +742,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     } else {
     int g = 0, seg = 0;
     int xk = 0;                                          // PAIR: logit exchanges done by this warp
+    pdl_wait();
     if (S.b_first <= S.b_last) load_q(S.b_first);
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
