@@ -90,6 +90,10 @@ constexpr int kSlots = 23;        // trace slots: qk_issue, pv_issue, s_ready, p
     if ((MODE & 2) && blockIdx.x == a.trace_cta && (gg) < kTrace) a.trace[(slot) * kTrace + (gg)] = clock64(); \
   } while (0)
 
+#ifndef TPLA_SEQ_COST_TOKENS
+#define TPLA_SEQ_COST_TOKENS 0      // 0: the measured per-width default (Cfg::SEQ_COST)
+#endif
+
 template <int W_LAT>
 struct Cfg {
   // PAIR (W_lat = 512: g = 1, plain MLA): O [128 x 512] fp32 alone would fill TMEM, so a cluster of
@@ -128,7 +132,12 @@ struct Cfg {
 #endif
   static constexpr int SUB = TT / kSub;               // TMA boxes per column group per tile
   static constexpr int CH = TT / 2;                   // S columns per softmax warp
-  static constexpr int SEQ_COST = 512 / TT;           // per-sequence header cost in tiles (schedule)
+  // Per-sequence header cost of the schedule, in tiles: a CTA whose range starts a second
+  // segment pays its epilogue, the next Q load and the pipeline refill.  Measured with the trace's
+  // per-CTA end times (h8, c1): at 512 tokens the two-segment CTAs ended 3-4 us after the others
+  // (every one of the slowest eight had two segments).  A/B of the in-step K3 time over 512 / 768 /
+  // 1024 / 1536 tokens: 1024 best at W_lat 64 / 256 (h8 -3.5 %, c1 -4 %, c3 -3 %), 512 at W_lat 128.
+  static constexpr int SEQ_COST = (TPLA_SEQ_COST_TOKENS > 0 ? TPLA_SEQ_COST_TOKENS : W_LAT == 128 ? 512 : 1024) / TT;
   static constexpr int W = WL + 64;
   static constexpr int NBOX = W / 64;                 // 64-column groups per tile (latent part + RoPE)
   static constexpr int SUB_BYTES = kSub * 128;        // one TMA box: 64 rows x 128 B
@@ -1069,6 +1078,9 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
                 cc[2 * c + 1] - cc[2 * c], 1e3 * double(cc[2 * c + 1] - cc[2 * c]) / double(en - st));
     }
     fprintf(stderr, "[k3 cta] span %lld ns, latest start %lld ns\n", t1 - t0, s_max);
+    fprintf(stderr, "[k3 ends]");                   // every CTA's end (ns), for balance analysis
+    for (int c = 0; c < n_cta; ++c) fprintf(stderr, " %lld", cs[2 * c + 1] - t0);
+    fprintf(stderr, "\n");
     fprintf(stderr, "[k3 cta] traced CTA: start -> qk_issue[0] %lld cycles, qk_issue[0] -> end %lld cycles\n",
             h[0] - cc[2 * b.trace_cta], cc[2 * b.trace_cta + 1] - h[0]);
     {
