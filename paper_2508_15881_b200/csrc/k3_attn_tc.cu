@@ -538,7 +538,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     const uint32_t pair_bar = 1 + q4;                   // named barrier of the two warps of a quadrant
     // Q'_j row -> TMEM (A operand, bf16 pairs per 32-bit column), half of it per warp;
     // q^PE row -> swizzled smem (chunks 4*half .. 4*half+3); then signal the MMA warp
+    // (the q^PE loads are issued first: the Q' TMEM stores are asm volatile with a memory clobber,
+    // so loads placed after them would wait for a second round trip)
     auto load_q = [&](int bb) {
+        const uint4* pe = reinterpret_cast<const uint4*>(
+            a.q_pe + (((long)bb * a.n_q + tok_i) * a.h_q + a.head_begin + head_h) * 64);
+        uint4 pev[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) pev[c] = row_ok ? pe[4 * half + c] : make_uint4(0, 0, 0, 0);
         const uint4* src = reinterpret_cast<const uint4*>(
             a.q_lat + (((long)bb * a.n_q + tok_i) * a.h_loc + head_h) * W_LAT + crank * C::WL);
         constexpr int QC = C::WL / 2;                   // packed columns of Q'_j
@@ -556,12 +563,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
             tmem_st32(lane_base + C::Q_COL + c_begin + c0, w);
           }
         }
-        const uint4* pe = reinterpret_cast<const uint4*>(
-            a.q_pe + (((long)bb * a.n_q + tok_i) * a.h_q + a.head_begin + head_h) * 64);
 #pragma unroll
-        for (int ch = 4 * half; ch < 4 * half + 4; ++ch) {
-          uint4 u = row_ok ? pe[ch] : make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(s_qpe + r * 128 + ((ch ^ (r & 7)) << 4)) = u;
+        for (int c = 0; c < 4; ++c) {
+          const int ch = 4 * half + c;
+          *reinterpret_cast<uint4*>(s_qpe + r * 128 + ((ch ^ (r & 7)) << 4)) = pev[c];
         }
         fence_proxy_async_smem();
         tmem_st_wait();
