@@ -11,11 +11,18 @@ namespace tpla {
 // its predecessor's completion + memory flush (pdl_wait) only before touching its outputs.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-// A kernel that does not read its predecessor's output (K1 append, K2 absorb) waits at its END
-// instead: it overlaps the predecessor, and its completion still implies the predecessor's, so
-// completion stays transitive along the stream for the kernels that wait at entry.
+// A kernel that does not read its predecessor's output (K1 append, K2 absorb) does its loads and
+// math under the predecessor's tail and waits right before its first global store: a store may
+// not overtake a still-running kernel that reads the same buffer (write-after-read: the previous
+// step's K3 re-reads Q' and the appended cache rows, K5 streams a v staged in the workspace).
+// Every thread waits once before it exits, so a grid's completion implies its predecessor's and
+// completion stays transitive along the stream.
 
 bool pdl_enabled();   // TPLA_PDL=0 disables (host)
+// Set before a launch that must not overlap its predecessor at all (plain stream order): the next
+// launch_kc on this thread omits the PDL attribute, then the flag clears.  Used where a kernel
+// reads, before its griddepcontrol.wait, data that the preceding kernel writes (K6's tables).
+extern thread_local bool g_no_pdl_next;
 
 // kernel<<<grid, block, smem, s>>>(args...) with the PDL launch attribute (and, when cluster_x > 1,
 // thread-block clusters of cluster_x consecutive CTAs)
@@ -29,7 +36,9 @@ cudaError_t launch_kc(void (*kernel)(KArgs...), int cluster_x, dim3 grid, dim3 b
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   int n = 0;
-  if (pdl_enabled()) {
+  const bool pdl = pdl_enabled() && !g_no_pdl_next;
+  g_no_pdl_next = false;
+  if (pdl) {
     at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[n++].val.programmaticStreamSerializationAllowed = 1;
   }

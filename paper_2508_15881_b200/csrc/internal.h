@@ -13,6 +13,7 @@ namespace tpla {
 
 extern std::atomic<int64_t> g_launches;
 extern std::atomic<int> g_profile_on;
+extern thread_local bool g_no_pdl_next;   // next launch without PDL (common.cuh)
 
 // Wraps one kernel launch: counts it (tpla_launch_count) and, when profiling is enabled
 // (tpla_profile_enable), brackets it with CUDA events on the launching stream.

@@ -37,8 +37,8 @@ __device__ __forceinline__ void append_row(const AppendArgs& a);
 template <int E>
 __global__ void __launch_bounds__(128) append_kernel(AppendArgs a) {
   pdl_trigger();
-  append_row<E>(a);
-  pdl_wait();   // inputs come from the host / earlier copies: wait only to keep completion transitive
+  append_row<E>(a);   // loads and math under the predecessor's tail; waits before its first store
+  pdl_wait();         // (threads without a row: keep completion transitive)
 }
 
 template <int E>
@@ -52,6 +52,7 @@ __device__ __forceinline__ void append_row(const AppendArgs& a) {
   if (seq >= 0 && seq < a.batch && p >= 0 && p < a.max_pages * a.page_size)
     page = a.block_table[(long)seq * a.max_pages + p / a.page_size];
   if (page < 0 || page >= a.num_pages) {
+    pdl_wait();
     if (lane == 0 && a.n_dropped) atomicAdd(a.n_dropped, 1);
     return;
   }
@@ -98,6 +99,7 @@ __device__ __forceinline__ void append_row(const AppendArgs& a) {
     if (a.rms_mode == TPLA_RMS_SLICED) r = rsqrtf(a.alpha / a.d_c * ss + a.eps);
     else if (a.rms_mode == TPLA_RMS_EXACT) r = rsqrtf(ss_full / a.d_c + a.eps);
     else r = 1.f;
+    pdl_wait();   // first store: the previous step's K3 may still read this row's 64-row box
     for (int l = lane; l < W; l += 32) {
       float acc = 0.f;
       for (int i = 0; i < a.d_c; ++i) acc = fmaf(c[i], a.xform[(long)i * W + l], acc);
@@ -138,6 +140,7 @@ __device__ __forceinline__ void append_row(const AppendArgs& a) {
     if (a.rms_mode == TPLA_RMS_SLICED) r = rsqrtf(a.alpha / a.d_c * ss + a.eps);
     else if (a.rms_mode == TPLA_RMS_EXACT) r = rsqrtf(ss_full / a.d_c + a.eps);
     else r = 1.f;
+    pdl_wait();   // first store: the previous step's K3 may still read this row's 64-row box
     if (mine) {
       uint16_t* o = dst + (e0 - a.lat_begin);
       if constexpr (E >= 8) {

@@ -25,7 +25,9 @@ struct GemmArgs {
   int M, N, K;
   // output: bf16 (out_bf16 != null) at out + z*o_zs + m*o_ms + n, else fp32 at out_f32 + ...
   uint16_t* out_bf16; float* out_f32; long o_zs, o_ms;
-  int inputs_from_host;   // 1: A/Bw are not written by the preceding kernel (PDL wait at the end)
+  int inputs_from_host;   // 1: A/Bw are not written by the preceding kernel (PDL wait before the stores)
+  int b_blocked;          // 1: Bw is W^O's blocked layout [ceil(N/128)][k_total/64][128][64] (tpla_convert_weights)
+  int b_ktiles;           // k_total / 64 of the blocked layout (z-slices start at z * K / 64)
 };
 
 __device__ __forceinline__ void nt_gemm_body(const GemmArgs& g);
@@ -36,8 +38,7 @@ __device__ __forceinline__ int swz(int row, int chunk) { return row * BK + ((chu
 __global__ void __launch_bounds__(THREADS) nt_gemm_kernel(GemmArgs g) {
   pdl_trigger();
   if (!g.inputs_from_host) pdl_wait();
-  nt_gemm_body(g);
-  if (g.inputs_from_host) pdl_wait();   // K2: q comes from the caller, wait only for transitivity
+  nt_gemm_body(g);   // (inputs_from_host: waits inside, after the math, before the first store)
 }
 
 __device__ __forceinline__ void nt_gemm_body(const GemmArgs& g) {
@@ -61,13 +62,16 @@ __device__ __forceinline__ void nt_gemm_body(const GemmArgs& g) {
       const uint16_t* src = ok ? A + (long)m * g.a_ms + k : A;
       cp_async16(sA + st * A_TILE + swz(r, ch), src, ok);
     }
-    // B: 128 rows x 8 chunks = 1024 chunks, 8 per thread
+    // B: 128 rows x 8 chunks = 1024 chunks, 8 per thread.  Blocked W^O: the [128 x 64] tile
+    // (row tile blockIdx.x, k tile z*K/64 + kt) is one contiguous 16 KB block
+    const uint16_t* bblk = g.b_blocked
+        ? g.Bw + ((long)blockIdx.x * g.b_ktiles + (long)z * (g.K / BK) + kt) * (BN * BK) : nullptr;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       int c = tid + i * THREADS, r = c >> 3, ch = c & 7;
       int n = n0 + r, k = k0 + ch * 8;
       bool ok = n < g.N && k < g.K;
-      const uint16_t* src = ok ? Bw + (long)n * g.b_ns + k : Bw;
+      const uint16_t* src = !ok ? g.Bw : g.b_blocked ? bblk + r * BK + ch * 8 : Bw + (long)n * g.b_ns + k;
       cp_async16(sB + st * B_TILE + swz(r, ch), src, ok);
     }
   };
@@ -117,6 +121,7 @@ __device__ __forceinline__ void nt_gemm_body(const GemmArgs& g) {
     }
   }
   cp_async_wait<0>();
+  if (g.inputs_from_host) pdl_wait();   // the first global store of a host-input GEMM (K2)
 
   // epilogue
 #pragma unroll
@@ -195,6 +200,11 @@ cudaError_t launch_skinny_gemm(const uint16_t* Wt, const uint16_t* v, int N, int
                                cudaStream_t s) {
   GemmArgs a{};
   const int Kc = K / kslices;
+  if (wo_blocked(K)) {                  // (the K-slices are 64-multiples: ws_layout)
+    if (Kc % BK) return cudaErrorInvalidValue;
+    a.b_blocked = 1;
+    a.b_ktiles = K / BK;
+  }
   a.A = v; a.a_zs = Kc; a.a_ms = K;
   a.Bw = Wt; a.b_zs = Kc; a.b_ns = K;
   a.M = B; a.N = N; a.K = Kc;

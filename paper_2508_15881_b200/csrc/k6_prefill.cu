@@ -5,7 +5,8 @@
 // (K2..K5) over pseudo-sequences: pseudo-sequence j holds the n_q prompt tokens
 // [r0 + j·n_q, r0 + (j+1)·n_q) as its newest tokens and attends causally to the first
 // r0 + (j+1)·n_q cached rows — all pseudo-sequences share the prompt's pages.  This kernel writes
-// their page-table rows (copies of the prompt's row) and lengths.
+// their page-table rows (copies of the prompt's row) and lengths.  The decode launch that follows
+// runs without PDL (tpla_prefill_attention): K3 reads the tables before its griddepcontrol.wait.
 #include <algorithm>
 
 #include "common.cuh"
@@ -18,13 +19,13 @@ __global__ void prefix_table_kernel(const int32_t* __restrict__ block_table, int
                                     int n_q, int r0, int n_rows, int32_t* __restrict__ table,
                                     int32_t* __restrict__ lens) {
   pdl_trigger();
+  pdl_wait();   // the previous call's K3 may still read this region (write-after-read)
   const int n_seq = n_full + (n_rows > n_full * n_q ? 1 : 0);
   const int32_t* src = block_table + long(seq) * max_pages;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_seq * max_pages; i += gridDim.x * blockDim.x)
     table[i] = src[i % max_pages];
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_seq; j += gridDim.x * blockDim.x)
     lens[j] = j < n_full ? r0 + (j + 1) * n_q : r0 + n_rows;
-  pdl_wait();   // (reads caller inputs only: wait for transitivity)
 }
 
 }  // namespace

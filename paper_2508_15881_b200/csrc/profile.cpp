@@ -17,6 +17,7 @@
 namespace tpla {
 
 std::atomic<int> g_profile_on{0};
+thread_local bool g_no_pdl_next = false;
 
 namespace {
 struct Pending {

@@ -205,6 +205,22 @@ SplitPlan choose_split(int B, int max_seq_len) {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// The tcgen05 W^O GEMM takes at most kWoRows output rows per launch (the MMA N of its swap-AB
+// tile): larger batches run as consecutive row chunks sharing the partial workspace (each
+// chunk's GEMM waits for the previous chunk's reduce before writing it: PDL wait at entry).
+constexpr int kWoRows = 256;
+static cudaError_t run_wo_tc(const uint16_t* Wo, const uint16_t* v, int D, int K, int R, void* part, float* y,
+                             bool accumulate, uint16_t* out16, cudaStream_t s, int k_begin = 0, int k_len = 0) {
+  const int kl = k_len > 0 ? k_len : K;             // v's row length (the K-slice's columns)
+  for (int r0 = 0; r0 < R; r0 += kWoRows) {
+    const int n = std::min(kWoRows, R - r0);
+    cudaError_t e = launch_wo_tc(Wo, v + size_t(r0) * kl, D, K, n, part, y + size_t(r0) * D, accumulate,
+                                 out16 ? out16 + size_t(r0) * D : nullptr, s, k_begin, k_len);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 WsLayout ws_layout(const Geom& g, int B, int n_q, int max_seq_len) {
   WsLayout L{};
   const int R = B * n_q;                                 // output rows (sequence, query token)
@@ -227,7 +243,7 @@ WsLayout ws_layout(const Geom& g, int B, int n_q, int max_seq_len) {
   L.v = off;       off += align256(size_t(R) * K * 2);
   L.y_part = off;  off += align256(size_t(L.kslices) * R * g.D * 4);
   L.meta = off;    off += align256(size_t(B) * 2 * 4);
-  L.wo_part = off; off += align256(wo_tc_supported(g.D, K, R) ? wo_tc_part_bytes(g.D, K, R) : 0);
+  L.wo_part = off; off += align256(wo_tc_supported(g.D, K, std::min(R, kWoRows)) ? wo_tc_part_bytes(g.D, K, std::min(R, kWoRows)) : 0);
   L.total = off;
   return L;
 }
@@ -261,7 +277,10 @@ static cudaError_t run_attention(const Geom& g, const tpla_cache& cache, const u
 // =====================================================================================
 extern "C" {
 
-const char* tpla_version(void) { return "tpla-b200 0.1 (sm_100a)"; }
+#ifndef TPLA_SRC_HASH
+#define TPLA_SRC_HASH "unknown"
+#endif
+const char* tpla_version(void) { return "tpla-b200 0.2 (sm_100a) src " TPLA_SRC_HASH; }
 const char* tpla_last_error(void) { return t_err.c_str(); }
 int64_t tpla_launch_count(void) { return g_launches.load(); }
 
@@ -448,6 +467,11 @@ static tpla_status append_common(const tpla_config* cfg, const tpla_weights* w, 
   if (n == 0) return ok();
   if (!c_kv || !k_pe || !seq_idx || !pos) return fail(TPLA_ERR_INVALID_ARG, "NULL input");
   if (!aligned16(c_kv)) return fail(TPLA_ERR_INVALID_ARG, "c_kv not 16-byte aligned");
+  // the Hadamard / identity cache write gives each lane d_c/32 consecutive latents: the device's
+  // slice must be whole lanes (g <= 32 at d_c = 1024, any g <= d_c/32 in general)
+  if (w->xform_kind != TPLA_XFORM_PCA && g.w_lat % (g.d_c / 32))
+    return fail(TPLA_ERR_UNSUPPORTED, "W_lat=%d: the cache-write kernel needs W_lat a multiple of d_c/32=%d", g.w_lat,
+                g.d_c / 32);
   cudaError_t e = launch_append_kv(g, w->xform_kind, static_cast<const float*>(w->xform), w->alpha_j, *cache,
                                    static_cast<const uint16_t*>(c_kv), static_cast<const uint16_t*>(k_pe), seq_idx,
                                    pos, n, rms_mode, n_dropped, static_cast<cudaStream_t>(stream));
@@ -564,10 +588,10 @@ tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const
   const int Kw = g.h_loc * g.d_h;
   const char* force = getenv("TPLA_WO");
   bool out_done = false;
-  if (wo_tc_supported(g.D, Kw, R) && !(force && strcmp(force, "mma") == 0)) {
+  if (wo_tc_supported(g.D, Kw, std::min(R, kWoRows)) && !(force && strcmp(force, "mma") == 0)) {
     // without an all-reduce the segment reduce also writes the bf16 output (no cast launch)
     uint16_t* out16 = comm ? nullptr : static_cast<uint16_t*>(out);
-    e = launch_wo_tc(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, R, base + L.wo_part, y, accumulate, out16, s);
+    e = run_wo_tc(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, R, base + L.wo_part, y, accumulate, out16, s);
     if (e != cudaSuccess) return cuda_fail(e, "K5b W_O (tcgen05)");
     out_done = out16 != nullptr;
   } else {
@@ -662,9 +686,14 @@ tpla_status tpla_prefill_attention(const tpla_config* cfg, const tpla_weights* w
       pc.batch = parts[k].n_seq;
       pc.block_table = table + size_t(k ? full : 0) * cache->max_pages_per_seq;
       const size_t r = size_t(parts[k].row0);
+      // K3 reads the pseudo-sequence table and lengths before its PDL wait (its schedule runs
+      // under the predecessor's tail), so the first launch after K6 (K2) waits for K6 in plain
+      // stream order; K3, launched after K2 started, then sees K6's writes.
+      g_no_pdl_next = k == 0;
       st = tpla_decode_mtp(cfg, w, &pc, qn + r * g.h_q * g.d_h, qp + r * g.h_q * g.d_r, lens + (k ? full : 0),
                            parts[k].n_seq, parts[k].n_q, L, base, p.dec_bytes, y + r * g.D, o16 ? o16 + r * g.D : nullptr,
                            flags, comm, stream);
+      g_no_pdl_next = false;
       if (st) return st;
     }
   }
@@ -726,14 +755,15 @@ tpla_status tpla_project_out(const tpla_config* cfg, const tpla_weights* w, floa
     return fail(TPLA_ERR_INVALID_ARG, "group communicator (rank %d of %d) must be chunk %d of %d", group_comm->rank,
                 group_comm->world, chunk, n_chunks);
   const int kc = K / n_chunks;
-  if (!wo_tc_supported(g.D, K, R))
+  if (!wo_tc_supported(g.D, K, std::min(R, kWoRows)))
     return fail(TPLA_ERR_UNSUPPORTED, "tpla_project_out needs the tcgen05 W^O path (K=%d, R=%d)", K, R);
   if (comm && (g.k % comm->world))
     return fail(TPLA_ERR_INVALID_ARG, "communicator world %d does not divide k=%d", comm->world, g.k);
   if ((group_comm || comm) && !load_nccl()) return fail(TPLA_ERR_NCCL, "NCCL not loadable");
   const size_t v_bytes = align256(size_t(R) * kc * 2);
-  if (ws_bytes < v_bytes + wo_tc_part_bytes(g.D, kc, R))
-    return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, v_bytes + wo_tc_part_bytes(g.D, kc, R));
+  const size_t part_bytes = wo_tc_part_bytes(g.D, kc, std::min(R, kWoRows));
+  if (ws_bytes < v_bytes + part_bytes)
+    return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, v_bytes + part_bytes);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   float* v_mine = v_acc + size_t(chunk) * R * kc;                  // chunk c: [R, kc] contiguous
   if (group_comm && n_chunks > 1) {                                // Σ over the group, chunk c to its rank
@@ -744,8 +774,8 @@ tpla_status tpla_project_out(const tpla_config* cfg, const tpla_weights* w, floa
   cudaError_t e = launch_cast_bf16(v_mine, long(R) * kc, v16, s, "K5_v_cast");           // v = bf16(Σ_j v_j), this slice
   if (e != cudaSuccess) return cuda_fail(e, "v cast");
   uint16_t* out16 = comm ? nullptr : static_cast<uint16_t*>(out);
-  e = launch_wo_tc(static_cast<const uint16_t*>(w->W_O), v16, g.D, K, R, static_cast<char*>(ws) + v_bytes, y,
-                   (flags & TPLA_DECODE_ACCUMULATE) != 0, out16, s, chunk * kc, kc);
+  e = run_wo_tc(static_cast<const uint16_t*>(w->W_O), v16, g.D, K, R, static_cast<char*>(ws) + v_bytes, y,
+                (flags & TPLA_DECODE_ACCUMULATE) != 0, out16, s, chunk * kc, kc);
   if (e != cudaSuccess) return cuda_fail(e, "K5b W_O (tcgen05)");
   if (comm) {                                                      // C1: O = AllReduce(Σ Õ)
     ncclResult_t r = g_nccl.AllReduce(y, y, size_t(R) * g.D, ncclFloat32, ncclSum, comm->comm, s);

@@ -204,8 +204,7 @@ class TplaRank:
     # ---- host view of the cache (tests)
     def cache_rows_bits(self, b: int, n: int) -> np.ndarray:
         """bf16 bits [n, row_stride] of sequence b's first n tokens, gathered through the page table."""
-        img = bits_from_bf16(self.cache_buf)
-        pages = self.block_table_host[b]
-        t = np.arange(n)
-        return img[pages[t // self.page_size], t % self.page_size]
+        t = torch.arange(n, device=self.cache_buf.device)
+        pages = self.block_table[b].long()[t // self.page_size]
+        return bits_from_bf16(self.cache_buf[pages, t % self.page_size])     # gathered on the device
 

@@ -42,6 +42,9 @@ def test_library_is_sm100a():
 
 def test_version_and_counter():
     assert "sm_100a" in abi.tpla_version()
+    # the loaded library was compiled from exactly this tree (build.py embeds the content hash)
+    from paper_2508_15881_b200 import build as b
+    assert abi.tpla_version().endswith("src " + b.source_hash())
     assert abi.tpla_launch_count() >= 0
 
 

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import synth
-from oracle import numerics, plan as oplan, reparam, tpla
+from oracle import mla, numerics, plan as oplan, reparam, tpla
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -228,16 +228,19 @@ def test_attention_parity_divergent_rescale():
 
 
 # ----------------------------------------------------------------------------- end to end (K1..K5)
-def e2e_case(d, dims, k, g, kind, S_list, *, seed=0, modes=("exact", "sliced"), check_rank_parts=True, wo="rank"):
+def e2e_case(d, dims, k, g, kind, S_list, *, seed=0, modes=("exact", "sliced"), check_rank_parts=True, wo="rank",
+             mu=None):
     """All k ranks of a (k, g) plan run on this GPU, each accumulating into y (k-shard emulation);
     compared with the oracle's full step (sum over ranks).
     wo: "rank"   every rank projects its own v_j through W^O (tpla_decode, P:139-141);
         "shared" the g ranks of a head block add their v_j into one v_acc, projected once (f2(ii));
         "split"  as if each rank of a group were its own process: v_acc in g column chunks per rank,
                  the group sum formed here (the reduce-scatter's arithmetic), each rank projecting
-                 its chunk's K-slice of W^O."""
+                 its chunk's K-slice of W^O.
+    mu: None = mu_j = alpha_j (reading R6), else a scalar for every shard (1.0: the literal §4 reading)."""
     B = len(S_list)
     xf, sseed, U, U32, alpha = transform_inputs(kind, dims, 21, g)
+    mu = np.asarray(alpha, float) if mu is None else np.full(g, float(mu))
     basis = U if kind == "pca" else None
     w = synth.gen_weights(dims, seed + 1)
     q, qpe = synth.gen_queries(dims, B, seed + 2)
@@ -250,7 +253,7 @@ def e2e_case(d, dims, k, g, kind, S_list, *, seed=0, modes=("exact", "sliced"), 
     for rid in range(k):
         r = TplaRank(spec_of(dims), k=k, g=g, rank=rid, batch=B, max_seq_len=max(S_list), device=d,
                      page_perm_seed=rid)
-        r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=xf, sign_seed=sseed, U_pca=U32, alpha=alpha)
+        r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=xf, sign_seed=sseed, U_pca=U32, alpha=alpha, mu=mu)
         seq = np.concatenate([np.full(n, b, np.int32) for b, n in enumerate(n_prompt)])
         pos = np.concatenate([np.arange(n, dtype=np.int32) for n in n_prompt])
         ck = np.concatenate([c_raw[b][:n] for b, n in enumerate(n_prompt)])
@@ -294,7 +297,7 @@ def e2e_case(d, dims, k, g, kind, S_list, *, seed=0, modes=("exact", "sliced"), 
     abi.tpla_sync(0)
     torch.cuda.synchronize()
     pb = tpla.Problem(W_UK=f64(w.W_UK), W_UV=f64(w.W_UV), gamma=f64(w.gamma), W_O=f64(w.W_O), U=U,
-                      alpha=np.asarray(alpha, float), mu=np.asarray(alpha, float),
+                      alpha=np.asarray(alpha, float), mu=mu,
                       c_raw=[f64(c) for c in c_raw], k_pe=[f64(x) for x in k_pe],
                       modes=[[tpla.EXACT] * n + [tpla.SLICED] * (S - n) for S, n in zip(S_list, n_prompt)],
                       q_nope=f64(q), q_pe=f64(qpe), h_q=dims.h_q, d_h=dims.d_h, eps=1e-6,
@@ -615,3 +618,130 @@ def test_e2e_parity_ragged_combine_blocks():
     S_list = [1 + (7 * b) % 97 for b in range(33)]
     e2e_case(dev(), synth.PRESETS["dsv3"], 2, 2, "hadamard", S_list)
     e2e_case(dev(), synth.PRESETS["dsv3"], 2, 2, "hadamard", S_list, wo="shared")
+
+
+# ----------------------------------------------------------------------------- round-2 parity cases
+@pytest.mark.parametrize("dname,k,g,kind", [("dsv3", 2, 2, "hadamard"), ("dsv3", 8, 8, "hadamard"),
+                                            ("kimi", 4, 4, "identity"), ("tiny", 2, 2, "pca")])
+def test_e2e_parity_mu_one(dname, k, g, kind):
+    """Reading R6's alternative: mu_j = 1 (the literal §4 equations, no NoPE logit scaling)."""
+    e2e_case(dev(), synth.PRESETS[dname], k, g, kind, [5, 200, 333], mu=1.0)
+    e2e_case(dev(), synth.PRESETS[dname], k, g, kind, [5, 200, 333], mu=1.0, wo="shared")
+
+
+def dup_slices_case(d, dims, k, g, S_list, *, seed=0, wo="rank"):
+    """Closed form (pin c8 at any g): c = [a ‖ a ‖ ... ‖ a] (g copies) and the W^UK / W^UV rows repeated
+    the same way, gamma = 1, identity U, alpha = mu = g.  Conditions 1 and 2 hold with equality
+    (P:201-209), so the GPU's sliced TPLA (every row appended SLICED by K1) must equal
+    plain MLA (oracle mla_decode_full, non-absorbed, g = 1) up to the bf16 storage."""
+    B = len(S_list)
+    wl = dims.d_c // g
+    w = synth.gen_weights(dims, seed + 1, gamma_one=True)
+    W_UK, W_UV = w.W_UK.copy(), w.W_UV.copy()
+    for j in range(1, g):
+        W_UK[j * wl:(j + 1) * wl] = W_UK[:wl]
+        W_UV[j * wl:(j + 1) * wl] = W_UV[:wl]
+    q, qpe = synth.gen_queries(dims, B, seed + 2)
+    c_raw = [np.concatenate([synth.gen_raw_ckv(dims, S, seed + 3, b)[:, :wl]] * g, axis=1) for b, S in enumerate(S_list)]
+    k_pe = [synth.gen_kpe(dims, S, seed + 3, b) for b, S in enumerate(S_list)]
+    lens = torch.tensor(S_list, dtype=torch.int32, device=d)
+    y = torch.zeros((B, dims.D), dtype=torch.float32, device=d)
+    ranks = []
+    for rid in range(k):
+        r = TplaRank(spec_of(dims), k=k, g=g, rank=rid, batch=B, max_seq_len=max(S_list), device=d,
+                     page_perm_seed=rid + 11)
+        r.convert(W_UK, W_UV, w.gamma, w.W_O, xform=abi.XFORM_IDENTITY, alpha=np.full(g, float(g)),
+                  mu=np.full(g, float(g)))
+        seq = np.concatenate([np.full(S, b, np.int32) for b, S in enumerate(S_list)])
+        pos = np.concatenate([np.arange(S, dtype=np.int32) for S in S_list])
+        r.append(bf16_from_bits(np.concatenate(c_raw), d), bf16_from_bits(np.concatenate(k_pe), d),
+                 torch.from_numpy(seq).to(d), torch.from_numpy(pos).to(d), abi.RMS_SLICED)
+        if wo == "rank":
+            r.decode(bf16_from_bits(q, d), bf16_from_bits(qpe, d), lens, y, accumulate=True)
+        ranks.append(r)
+    if wo == "shared":
+        for hb in sorted({r.plan.head_block for r in ranks}):
+            grp = [r for r in ranks if r.plan.head_block == hb]
+            acc = torch.zeros(grp[0].v_acc_shape(B), dtype=torch.float32, device=d)
+            for j, r in enumerate(grp):
+                r.decode_v(bf16_from_bits(q, d), bf16_from_bits(qpe, d), lens, acc, accumulate=j > 0)
+            grp[0].project_out(acc, y, accumulate=True)
+    torch.cuda.synchronize()
+    ref = np.stack([mla.mla_decode_full(f64(q[b]), f64(qpe[b]), f64(c_raw[b]), f64(k_pe[b]), f64(W_UK), f64(W_UV),
+                                        f64(w.gamma), f64(w.W_O), h_q=dims.h_q, d_h=dims.d_h, eps=1e-6,
+                                        sm_scale=dims_scale(dims))[0] for b in range(B)])
+    e = row_rel_err(y.cpu().numpy(), ref)
+    assert e <= TOL, e
+    return e
+
+
+@pytest.mark.parametrize("k,g", [(2, 2), (4, 4), (8, 8), (8, 4)])
+@pytest.mark.parametrize("wo", ["rank", "shared"])
+def test_duplicated_slices_tpla_equals_mla(k, g, wo):
+    """The alpha = g / mu = alpha chain at g = 4 and 8 (C2, C3, the 8-GPU headline) on the GPU,
+    against MLA itself (DeepSeek-V3 shape)."""
+    dup_slices_case(dev(), synth.PRESETS["dsv3"], k, g, [3, 130, 257], wo=wo)
+
+
+@pytest.mark.parametrize("k,g", [(2, 2), (8, 8)])
+def test_full_size_decode_v_project_out_all_sequences(k, g):
+    """The production path at full size, in the bench's launch configuration: configs[1] (k = g = 2)
+    and the 8-GPU 32K headline shape (k = g = 8), batch 32, 32K context, every rank co-located on
+    this GPU: K2 -> K3 -> K45 (decode_v, the group's v summed in place) -> K5 (project_out).  The
+    cache rows are seeded N(0, 1) bf16 rows (torch Philox); ALL 32 sequences are checked against
+    the oracle (absorb, shard attention, W^UV, W^O, sum over ranks) on those rows."""
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    B, S = 32, 32768
+    w = synth.gen_weights(dims, 77)
+    q, qpe = synth.gen_queries(dims, B, 78)
+    lens_h = np.full(B, S, np.int32)
+    lens_h[5] = S - 1000
+    lens_h[17] = 4097
+    lens = torch.from_numpy(lens_h).to(d)
+    U = reparam.hadamard_U(dims.d_c, 79)
+    gen = torch.Generator(device=d)
+    gen.manual_seed(80)
+    ranks = []
+    for rid in range(k):
+        r = TplaRank(spec_of(dims), k=k, g=g, rank=rid, batch=B, max_seq_len=S, device=d)
+        r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_HADAMARD, sign_seed=79)
+        r.cache_buf[..., :r.plan.row_width].normal_(generator=gen)
+        ranks.append(r)
+    y = torch.zeros((B, dims.D), dtype=torch.float32, device=d)
+    acc = torch.zeros(ranks[0].v_acc_shape(B), dtype=torch.float32, device=d)
+    qd, qped = bf16_from_bits(q, d), bf16_from_bits(qpe, d)
+    for j, r in enumerate(ranks):          # k = g: one head block, the whole latent group on this GPU
+        r.decode_v(qd, qped, lens, acc, accumulate=j > 0)
+    ranks[0].project_out(acc, y)
+    torch.cuda.synchronize()
+    got = y.cpu().numpy()
+    W_UK_new, W_UV_new = tpla.reparam_weights(f64(w.W_UK), f64(w.W_UV), f64(w.gamma), U)
+    alpha = np.full(g, float(g))
+    eye = np.eye(dims.d_c)
+    plans = [oplan.make_plan(k, g, dims.h_q, dims.d_c, dims.d_r, r.rank) for r in ranks]
+    W_O = f64(w.W_O)
+    dws = [tpla.convert_weights(W_UK_new, W_UV_new, np.ones(dims.d_c), W_O, eye, pl, alpha[pl.shard], d_h=dims.d_h)
+           for pl in plans]
+    qf, qpef = f64(q), f64(qpe)
+    ref = np.zeros((B, dims.D))
+    for b in range(B):
+        for r, pl, dw in zip(ranks, plans, dws):
+            rows = f64(r.cache_rows_bits(b, int(lens_h[b]))[:, :pl.row_width])
+            ref[b] += tpla.decode_device(qf[b:b + 1], qpef[b:b + 1], [rows], dw, pl, sm_scale=dims_scale(dims))[0]
+    e = row_rel_err(got, ref)
+    assert e <= TOL, e
+
+
+def test_wo_large_batch_row_chunks():
+    """B = 300 > 256 output rows: the tcgen05 W^O GEMM runs in 256-row chunks (decode and project_out)."""
+    S_list = [1 + (13 * b) % 41 for b in range(300)]
+    e2e_case(dev(), synth.PRESETS["dsv3"], 2, 2, "hadamard", S_list)
+    e2e_case(dev(), synth.PRESETS["dsv3"], 2, 2, "hadamard", S_list, wo="shared")
+
+
+def test_wo_mma_baseline_reads_blocked_layout(monkeypatch):
+    """TPLA_WO=mma (the mma.sync W^O baseline) reads the blocked W^O layout tpla_convert_weights writes."""
+    monkeypatch.setenv("TPLA_WO", "mma")
+    e2e_case(dev(), synth.PRESETS["dsv3"], 2, 2, "hadamard", [5, 200, 333])
+    e2e_case(dev(), synth.PRESETS["dsv3"], 8, 2, "identity", [64, 129])

@@ -269,16 +269,21 @@ def test_c4_shard_softmax_rows_and_rope(k, g):
                 assert np.array_equal(a, b)
 
 
-# ---------------------------------------------------------------- c8: duplicated halves
-def _dup_problem(dims, mu):
-    pb = make_problem(dims, g=2, S=29)
-    h = dims.d_c // 2
+# ---------------------------------------------------------------- c8: duplicated slices
+def _dup_problem(dims, mu, g=2):
+    """c' = [a ‖ a ‖ ... ‖ a] and W^UK / W^UV rows repeated the same way (g copies), gamma = 1:
+    every slice carries 1/g of the energy, so alpha = g makes the sliced RMS the full RMS
+    (Condition 1 with equality) and each shard's NoPE logit is 1/g of MLA's, which
+    mu = g restores (Condition 2 with equality)."""
+    pb = make_problem(dims, g=g, S=29)
+    w = dims.d_c // g
     pb.gamma = np.ones(dims.d_c)
     for arr in (pb.W_UK, pb.W_UV):
-        arr[h:] = arr[:h]                        # Q' = [b ‖ b]
-    pb.c_raw = [np.concatenate([c[:, :h], c[:, :h]], axis=1) for c in pb.c_raw]   # c' = [a ‖ a]
-    pb.mu = np.array([mu, mu], float)
-    pb.alpha = np.array([2.0, 2.0])
+        for j in range(1, g):
+            arr[j * w:(j + 1) * w] = arr[:w]     # Q' = [b ‖ b ‖ ...]
+    pb.c_raw = [np.concatenate([c[:, :w]] * g, axis=1) for c in pb.c_raw]   # c' = [a ‖ a ‖ ...]
+    pb.mu = np.full(g, float(mu))
+    pb.alpha = np.full(g, float(g))
     return pb
 
 
@@ -291,6 +296,61 @@ def test_c8_duplicated_halves_closed_form(dims):
     # the literal-§4 reading mu = 1 (no logit scaling) does not reach MLA
     pb1 = _dup_problem(dims, mu=1.0)
     assert rel(tpla.tpla_decode_step(pb1, 2, 2), mla_ref(pb1)) > 1e-2
+
+
+@pytest.mark.parametrize("g", [4, 8])
+@pytest.mark.parametrize("k_per_g", [1, 2])
+def test_c8_duplicated_slices_g4_g8(g, k_per_g):
+    """The alpha = g sliced-RMS / mu = alpha chain at g > 2 (configs C2, C3, the 8-GPU headline):
+    with g duplicated slices TPLA(k, g) equals MLA exactly (eps included); with mu = 1 each shard's
+    NoPE logits are 1/g too small and the output is O(1) off."""
+    dims = synth.PRESETS["odd"] if g == 4 else synth.PRESETS["tiny"]
+    if dims.h_q % k_per_g:
+        pytest.skip("heads do not split")
+    k = g * k_per_g
+    pb = _dup_problem(dims, mu=float(g), g=g)
+    assert rel(tpla.tpla_decode_step(pb, k, g), mla_ref(pb, absorbed=False)) < 1e-12
+    pb1 = _dup_problem(dims, mu=1.0, g=g)
+    assert rel(tpla.tpla_decode_step(pb1, k, g), mla_ref(pb1)) > 1e-2
+
+
+# ---------------------------------------------------------------- shard_attention's lse
+def test_lse_two_token_hand_case():
+    """Logits (0, ln 3) by construction (one head, one latent, no RoPE, scale 1):
+    lse = ln(1 + 3) = ln 4, p = (1/4, 3/4), O = 3/4 · 1 (hand-computed)."""
+    Qp = np.array([[np.log(3.0)]])
+    rows = np.array([[0.0], [1.0]])                       # ĉ_0 = 0, ĉ_1 = 1; d_r = 0
+    O, lse, p, _ = tpla.shard_attention(Qp, np.zeros((1, 0)), rows, 1, 1.0)
+    assert lse[0] == pytest.approx(np.log(4.0), rel=1e-15)
+    assert np.allclose(p[0], [0.25, 0.75], rtol=1e-15, atol=0)
+    assert O[0, 0] == pytest.approx(0.75, rel=1e-15)
+
+
+@pytest.mark.parametrize("S", [1, 7, 4096])
+def test_lse_uniform_logits_is_log_S(S):
+    """All logits equal to c (q = 0 and q^PE = 0 give c = 0; a constant RoPE logit shifts it):
+    lse = c + ln S, p = 1/S, O = the mean row."""
+    rng = np.random.default_rng(S)
+    H, W_lat, d_r = 3, 8, 4
+    rows = np.concatenate([rng.standard_normal((S, W_lat)), np.ones((S, d_r))], axis=1)
+    qpe = np.zeros((H, d_r))
+    qpe[1] = 0.5                                          # head 1: RoPE logit 4 * 0.5 = 2 on every token
+    O, lse, p, _ = tpla.shard_attention(np.zeros((H, W_lat)), qpe, rows, W_lat, 1.0)
+    assert np.allclose(lse, [np.log(S), 2.0 + np.log(S), np.log(S)], rtol=1e-14, atol=1e-14)
+    assert np.allclose(p, 1.0 / S, rtol=1e-12, atol=0)
+    assert np.allclose(O, rows[:, :W_lat].mean(axis=0)[None, :], rtol=1e-10, atol=1e-12)
+
+
+def test_lse_shift_and_large_logits():
+    """lse(s + c) = lse(s) + c, finite for logits near 700 where exp overflows (the stable form)."""
+    rng = np.random.default_rng(5)
+    rows = rng.standard_normal((50, 4))
+    Qp = rng.standard_normal((2, 4))
+    _, l0, _, _ = tpla.shard_attention(Qp, np.zeros((2, 0)), rows, 4, 1.0)
+    rows_c = np.concatenate([rows, np.full((50, 1), 1.0)], axis=1)
+    _, l1, _, _ = tpla.shard_attention(Qp, np.full((2, 1), 700.0), rows_c, 4, 1.0)
+    assert np.all(np.isfinite(l1))
+    assert np.allclose(l1 - l0, 700.0, rtol=1e-14, atol=1e-9)
 
 
 # ---------------------------------------------------------------- c9: degenerate softmax
