@@ -49,6 +49,7 @@ struct WsLayout {
   size_t v;         // bf16 [B, H_loc*d_h]
   size_t y_part;    // fp32 [kslices, B, D]
   size_t meta;      // int32 [B, 2] (persistent K3: first segment id, count)
+  size_t plan;      // int32 K3p schedule (attn_plan_bytes)
   size_t wo_part;   // persistent W^O GEMM partials + segment map
   size_t total;
   int kslices;
@@ -82,9 +83,14 @@ bool tc_attention_supported(const Geom& g, int B);
 // persistent K3 grid in logical CTAs (a logical CTA is a cluster of two for W_lat = 512)
 int tc_num_ctas(const Geom& g, int B, int max_seq_len);
 // n_q query tokens per sequence (multi-token decode): MMA rows = n_q * H_loc <= 128
+// K3p: the persistent K3's schedule (every CTA's tile range, segment base, first 32 box rows), computed
+// by one CTA from seq_lens and the block table ahead of K2; `plan`: attn_plan_bytes(n_cta, B) bytes
+size_t attn_plan_bytes(int n_cta, int B);
+cudaError_t launch_attn_plan(const Geom& g, const tpla_cache& cache, const int32_t* seq_lens, int B, int n_cta,
+                             int32_t* plan, cudaStream_t s);
 cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
-                                  const int32_t* seq_lens, int B, int n_q, int n_cta, float* o_part, float* ml_part,
-                                  int32_t* meta, cudaStream_t s);
+                                  const int32_t* seq_lens, int B, int n_q, int n_cta, const int32_t* plan,
+                                  float* o_part, float* ml_part, int32_t* meta, cudaStream_t s);
 cudaError_t launch_combine_seg(const Geom& g, int B, const float* o_part, const float* ml_part, const int32_t* meta,
                                uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s);
 

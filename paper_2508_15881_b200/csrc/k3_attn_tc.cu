@@ -47,6 +47,7 @@ constexpr int kSub = 64;          // cache rows per TMA box (page_size is a mult
 constexpr int kThreads = 384;    // w0 TMA, w1 MMA, w2 TMEM alloc, w3 schedule, w4-w11 softmax
 constexpr int kMaxB = 512;        // sequences per launch supported by the smem schedule
 constexpr int kMaxCta = 256;      // persistent grid bound (<= #SMs in practice)
+constexpr int kPlanStride = 8;    // ints per CTA entry of the K3p plan
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: p <= 2^8 between max updates
 // Every kPolyEvery-th group of 4 exponentials computes 2 of them with ex2_poly2 on the FMA pipe
 // (0 = none).  Measured (tools/gpu_variants.sh): at W_lat <= 128 a 1-in-8 share takes ~3 % off K3
@@ -62,6 +63,7 @@ struct TcArgs {
   const uint16_t* q_pe;        // [B, h_q, d_r]
   const int32_t* block_table;  // [B, max_pages]
   const int32_t* seq_lens;     // [B]
+  const int32_t* plan;         // K3p's schedule (plan_ints): per-CTA ranges, first box rows, cum, slen
   float* o_part;               // [max_segs, H_loc, W_lat]
   float* ml_part;              // [max_segs, H_loc, 2]
   int32_t* meta;               // [B, 2]: first segment id, segment count
@@ -189,6 +191,109 @@ __device__ __forceinline__ int upper_bound_cum(const int* cum, int n, int x) {  
   return lo;
 }
 
+// ---------------------------------------------------------------- K3p: the persistent schedule
+// Plan layout (int32, plan_ints(n_cta, B)): [n_cta][kPlanStride] = (lo, hi, b_first, b_last, seg_base),
+// then cum[B + 1], slen[B], then the first 32 box rows of every CTA [n_cta][32].
+struct PlanArgs {
+  const int32_t* seq_lens;
+  const int32_t* block_table;
+  int32_t* plan;
+  int B, n_cta, cap, page_size, max_pages;
+};
+
+__device__ __forceinline__ int block_excl_scan(int x, int* wsum, int& total) {   // 512 threads
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < 16 ? wsum[lane] : 0, wi = w;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < 16) wsum[16 + lane] = wi - w;          // exclusive warp offsets
+    if (lane == 15) wsum[32] = wi;
+  }
+  __syncthreads();
+  total = wsum[32];
+  const int r = wsum[16 + warp] + inc - x;
+  __syncthreads();                                   // (wsum reusable)
+  return r;
+}
+
+// One CTA (512 threads) computes the schedule of every K3 CTA: the flattened (sequence, tile) list
+// cut into equal work ranges with a per-sequence header cost (tile_of), each CTA's first segment id,
+// and its first 32 box rows through the page table.  It reads only caller inputs, so it runs under
+// the predecessor's tail (K1) and waits only before its stores.
+template <int W_LAT>
+__global__ void __launch_bounds__(512) attn_plan_kernel(PlanArgs p) {
+  pdl_trigger();
+  using C = Cfg<W_LAT>;
+  __shared__ int cum[kMaxB + 1], slen[kMaxB], lo_arr[kMaxCta + 1], wsum[40];
+  const int tid = threadIdx.x;
+  const int len = tid < p.B ? min(p.seq_lens[tid], p.cap) : 0;
+  const int nt = (len + C::TT - 1) / C::TT;
+  int total;
+  const int ex = block_excl_scan(nt, wsum, total);
+  if (tid < p.B) { cum[tid] = ex; slen[tid] = len; }
+  if (tid == 0) cum[p.B] = total;
+  __syncthreads();
+  const int n = p.n_cta;
+  const long Wt = long(total) + long(C::SEQ_COST) * p.B;            // total work units
+  for (int cc = tid; cc <= n; cc += 512) lo_arr[cc] = tile_of<C::SEQ_COST>(cum, p.B, cc * Wt / n);
+  __syncthreads();
+  int lo = 0, hi = 0, bf = 0, bl = -1;
+  if (tid < n) {
+    lo = lo_arr[tid];
+    hi = lo_arr[tid + 1];
+    if (lo < hi) {
+      bf = upper_bound_cum(cum, p.B + 1, lo) - 1;
+      bl = upper_bound_cum(cum, p.B + 1, hi - 1) - 1;
+    }
+  }
+  int n_seg_total;
+  const int seg_base = block_excl_scan(tid < n ? bl - bf + 1 : 0, wsum, n_seg_total);
+  // first 32 box rows of every CTA (the producer's first batch), resolved before the wait
+  constexpr int kPer = kMaxCta * 32 / 512;
+  int rows[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int idx = tid + i * 512, cc = idx >> 5, u = idx & 31;
+    rows[i] = 0;
+    if (cc < n) {
+      const int tt = lo_arr[cc] + u / C::SUB;
+      if (tt < lo_arr[cc + 1]) {
+        const int bb = upper_bound_cum(cum, p.B + 1, tt) - 1;
+        const int tok0 = (tt - cum[bb]) * C::TT;
+        int tok = tok0 + (u % C::SUB) * kSub;
+        if (tok >= slen[bb]) tok = tok0;
+        rows[i] = p.block_table[(long)bb * p.max_pages + tok / p.page_size] * p.page_size + tok % p.page_size;
+      }
+    }
+  }
+  pdl_wait();   // first store: the previous launch's K3 read this plan (write-after-read)
+  if (tid < n) {
+    int32_t* e = p.plan + tid * kPlanStride;
+    e[0] = lo; e[1] = hi; e[2] = bf; e[3] = bl; e[4] = seg_base;
+  }
+  int32_t* pc = p.plan + n * kPlanStride;
+  for (int i = tid; i <= p.B; i += 512) pc[i] = cum[i];
+  for (int i = tid; i < p.B; i += 512) pc[p.B + 1 + i] = slen[i];
+  int32_t* pr = pc + 2 * p.B + 1;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int idx = tid + i * 512;
+    if ((idx >> 5) < n) pr[idx] = rows[i];
+  }
+}
+
 // MODE 0: the kernel.  MODE 1 (diagnostic, TPLA_K3_MODE=stream): the TMA ring alone — every
 // tile is released as soon as it lands, no MMA/softmax — to measure the cache streaming rate.
 // Bit 16 (nosm, PP only): the softmax warps pass every tile straight through (MMA + ring alone).
@@ -213,8 +318,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   __shared__ uint32_t tmem_base;
   __shared__ int cum[kMaxB + 1];
   __shared__ int slen[kMaxB];            // min(seq_len, capacity) per sequence
-  __shared__ int lo_arr[kMaxCta + 1];    // first tile of every CTA's range (+ the end)
-  __shared__ int s_before;
+  __shared__ int s_sched[5];             // this CTA's plan entry: lo, hi, b_first, b_last, seg_base
   __shared__ float red_max[C::NSB][2][128];   // [S buffer][half][row] partial row maxima
   __shared__ float red_l[2][128];        // [half][row] partial row sums at a segment end
   __shared__ float red_m[2][128];        // PP: [set][row] the max each set's sums are expressed in
@@ -238,68 +342,34 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   }
   if (C::PAIR) cluster_sync();   // the peer's barriers are initialised before any remote operation
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(&tmem_base);
-  if (tid == 0) s_before = 0;
-  // The schedule and the page-table lookups read only caller inputs (seq_lens, the block table:
-  // their writes must be complete before tpla_decode is called, tpla.h), so they run before the
-  // PDL wait, overlapping the predecessor's tail; the wait comes right before the first read of a
-  // predecessor's output — the producer's first TMA (the cache rows K1 appended) and the softmax
-  // warps' first Q' load (K2) — and before any write (the epilogue's partials, read by the
-  // previous step's K45).  The MMA warps only consume what those threads hand over.
+  // The schedule (every CTA's tile range, segment ids, its first 32 box rows) was computed by K3p
+  // ahead of K2 (attn_plan_kernel): a CTA reads its entry and starts streaming.  (Computed here, the
+  // sequence scan, the range starts and the first page-table lookups took ~10 K cycles per CTA
+  // before the first TMA — measured, trace mode — with the SMs' HBM streams idle.)
   if (threadIdx.x == 0) EV(1);
-  if (warp == 3) {
-    // tiles per sequence -> exclusive prefix sum (warp scan, 32 sequences per step)
-    int carry = 0;
-    for (int b0 = 0; b0 < a.B; b0 += 32) {
-      int b = b0 + lane;
-      const int len = b < a.B ? min(a.seq_lens[b], a.cap) : 0;
-      if (b < a.B) slen[b] = len;
-      int t = (len + C::TT - 1) / C::TT;
-      int x = t;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (b < a.B) cum[b] = carry + x - t;
-      carry += __shfl_sync(0xffffffffu, x, 31);
-    }
-    if (lane == 0) cum[a.B] = carry;
-  }
-  __syncthreads();
-  // Every CTA needs the ranges of all CTAs before it (its first segment id = the number of
-  // segments they produce).  All threads share that work — one range start per thread — so no
-  // CTA pays a serial loop over its predecessors (that loop staggered the CTA starts by up to
-  // 6.7 us at 148 CTAs).
+  pdl_wait();          // the plan (K3p), Q' (K2) and the appended rows (K1) come from the predecessors
   {
-    const long Wt = long(cum[a.B]) + long(C::SEQ_COST) * a.B;     // total work units
-    for (int cc = tid; cc <= n_cta; cc += kThreads) lo_arr[cc] = tile_of<C::SEQ_COST>(cum, a.B, cc * Wt / n_cta);
-  }
-  __syncthreads();
-  {
-    int before = 0;
-    for (int cc = tid; cc < c; cc += kThreads) {
-      const int lo = lo_arr[cc], hi = lo_arr[cc + 1];
-      if (lo < hi) before += upper_bound_cum(cum, a.B + 1, hi - 1) - upper_bound_cum(cum, a.B + 1, lo) + 1;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
-    if (lane == 0 && before) atomicAdd(&s_before, before);
+    const int32_t* pl = a.plan;
+    const int off_cum = n_cta * kPlanStride, off_slen = off_cum + a.B + 1;
+    for (int i = tid; i <= a.B; i += kThreads) cum[i] = pl[off_cum + i];
+    for (int i = tid; i < a.B; i += kThreads) slen[i] = pl[off_slen + i];
+    if (tid < 5) s_sched[tid] = pl[c * kPlanStride + tid];
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) EV(11);
   if ((MODE & 2) && tid == 0) {
     a.trace[kSlots * kTrace + 2 * c] = globaltimer();
     a.trace[kSlots * kTrace + 2 * kMaxCta + 2 * c] = clock64();
   }
   const uint32_t tb = tmem_base;
   Sched S;
-  S.lo = lo_arr[c];
-  S.hi = lo_arr[c + 1];
-  S.b_first = S.lo < S.hi ? upper_bound_cum(cum, a.B + 1, S.lo) - 1 : 0;
-  S.b_last = S.lo < S.hi ? upper_bound_cum(cum, a.B + 1, S.hi - 1) - 1 : -1;
-  S.seg_base = s_before;
-
+  S.lo = s_sched[0];
+  S.hi = s_sched[1];
+  S.b_first = s_sched[2];
+  S.b_last = s_sched[3];
+  S.seg_base = s_sched[4];
 
   if (warp == 0) {
     // ============================================================ TMA producer (converged warp, one issuer)
@@ -319,9 +389,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       return a.block_table[(long)bb * a.max_pages + tok / a.page_size] * a.page_size + tok % a.page_size;
     };
     if (lane == 0) EV(2);
-    int rows_cur = lookup(lane), rows_next = lookup(32 + lane);
-    if (__shfl_sync(0xffffffffu, rows_cur + rows_next, 0) >= 0 && lane == 0) EV(3);
-    pdl_wait();
+    int rows_cur = a.plan[n_cta * kPlanStride + a.B + 1 + a.B + c * 32 + lane];   // K3p resolved the first 32
+    int rows_next = lookup(32 + lane);                 // (in flight while the first batch streams)
+    if (lane == 0) EV(3);
     for (int t = S.lo, g = 0; t < S.hi; ++t, ++g) {
       const int u0 = g * C::SUB;                       // SUB divides 32: a tile never spans batches
       if (u0 > 0 && (u0 & 31) == 0) {
@@ -360,7 +430,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         __syncwarp();
       }
   } else if (MODE == 1) {
-    pdl_wait();
     if (warp == 4 && lane == 0) {   // keep K4's segment map valid (values are meaningless)
       int seg = 0;
       for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
@@ -624,7 +693,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       return (a0 + a1) + (a2 + a3);
     };
     int g = 0, seg = 0;
-    pdl_wait();
     if (S.b_first <= S.b_last) load_q(S.b_first);
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
@@ -708,7 +776,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[sb]);
         if (t + 1 < t1) {                                // the other warp finalises tile g+1 next
+#ifndef TPLA_K3_NO_FENCE
           __threadfence_block();
+#endif
           named_bar_arrive(fin_mine, 64);
         }
       }
@@ -756,7 +826,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     } else {
     int g = 0, seg = 0;
     int xk = 0;                                          // PAIR: logit exchanges done by this warp
-    pdl_wait();
     if (S.b_first <= S.b_last) load_q(S.b_first);
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
@@ -1090,9 +1159,10 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
             h[0] - cc[2 * b.trace_cta], cc[2 * b.trace_cta + 1] - h[0]);
     {
       const long long* ev = h + kSlots * kTrace + 4 * kMaxCta;
-      fprintf(stderr, "[k3 start] cycles from kernel entry: pdl_wait %lld, sched %lld, lookups %lld, tma0 %lld, "
+      fprintf(stderr, "[k3 start] cycles from kernel entry: setup %lld, producer %lld, lookups %lld, tma0 %lld, "
               "q_loaded %lld, mma_q %lld, mma_kv0 %lld, qk0 %lld\n", ev[1] - ev[0], ev[2] - ev[0], ev[3] - ev[0],
               ev[4] - ev[0], ev[5] - ev[0], ev[6] - ev[0], ev[7] - ev[0], h[0] - ev[0]);
+      fprintf(stderr, "[k3 start] plan loaded %lld\n", ev[11] - ev[0]);
     }
     fprintf(stderr, "[k3 trace] g qk_issue qk_issued s_ready p_done pv_issue pv_issued (cycles rel. to qk_issue[0])\n");
     for (int g = 0; g < kTrace; ++g)
@@ -1145,9 +1215,33 @@ int tc_num_ctas(const Geom& g, int B, int max_seq_len) {
   return int(std::max(1L, std::min<long>(std::min(slots, kMaxCta), boxes / kMinBoxes)));
 }
 
+size_t attn_plan_bytes(int n_cta, int B) {
+  return size_t(n_cta) * (kPlanStride + 32) * 4 + size_t(2 * B + 1) * 4;
+}
+
+template <int W_LAT>
+cudaError_t launch_plan_w(const PlanArgs& p, cudaStream_t s) {
+  KernelScope ks("K3p_attn_plan", s);
+  return launch_k(attn_plan_kernel<W_LAT>, 1, 512, 0, s, p);
+}
+
+cudaError_t launch_attn_plan(const Geom& g, const tpla_cache& cache, const int32_t* seq_lens, int B, int n_cta,
+                             int32_t* plan, cudaStream_t s) {
+  if (B > kMaxB || n_cta > kMaxCta) return cudaErrorInvalidValue;
+  PlanArgs p{seq_lens, cache.block_table, plan, B, n_cta, cache.max_pages_per_seq * cache.page_size, cache.page_size,
+             cache.max_pages_per_seq};
+  switch (g.w_lat) {
+    case 64: return launch_plan_w<64>(p, s);
+    case 128: return launch_plan_w<128>(p, s);
+    case 256: return launch_plan_w<256>(p, s);
+    case 512: return launch_plan_w<512>(p, s);
+  }
+  return cudaErrorNotSupported;
+}
+
 cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
-                                  const int32_t* seq_lens, int B, int n_q, int n_cta, float* o_part, float* ml_part,
-                                  int32_t* meta, cudaStream_t s) {
+                                  const int32_t* seq_lens, int B, int n_q, int n_cta, const int32_t* plan,
+                                  float* o_part, float* ml_part, int32_t* meta, cudaStream_t s) {
   EncodeFn enc = get_encode();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap map;
@@ -1161,6 +1255,7 @@ cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const 
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   TcArgs a;
   a.q_lat = q_lat; a.q_pe = q_pe; a.block_table = cache.block_table; a.seq_lens = seq_lens;
+  a.plan = plan;
   a.o_part = o_part; a.ml_part = ml_part; a.meta = meta;
   a.B = B; a.h_loc = g.h_loc; a.h_q = g.h_q; a.head_begin = g.head_begin; a.page_size = cache.page_size;
   a.max_pages = cache.max_pages_per_seq; a.scale_log2 = g.sm_scale * 1.4426950408889634f;

@@ -243,6 +243,7 @@ WsLayout ws_layout(const Geom& g, int B, int n_q, int max_seq_len) {
   L.v = off;       off += align256(size_t(R) * K * 2);
   L.y_part = off;  off += align256(size_t(L.kslices) * R * g.D * 4);
   L.meta = off;    off += align256(size_t(B) * 2 * 4);
+  L.plan = off;    off += align256(attn_plan_bytes(L.n_cta, B));
   L.wo_part = off; off += align256(wo_tc_supported(g.D, K, std::min(R, kWoRows)) ? wo_tc_part_bytes(g.D, K, std::min(R, kWoRows)) : 0);
   L.total = off;
   return L;
@@ -262,7 +263,10 @@ static cudaError_t run_attention(const Geom& g, const tpla_cache& cache, const u
   cudaError_t e;
   if (use_tc_attention(g, B)) {
     auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
-    e = launch_decode_attn_tc(g, cache, q_lat, q_pe, seq_lens, B, 1, L.n_cta, o_part, ml_part, meta, s);
+    auto* plan = reinterpret_cast<int32_t*>(base + L.plan);
+    e = launch_attn_plan(g, cache, seq_lens, B, L.n_cta, plan, s);
+    if (e != cudaSuccess) return e;
+    e = launch_decode_attn_tc(g, cache, q_lat, q_pe, seq_lens, B, 1, L.n_cta, plan, o_part, ml_part, meta, s);
     if (e != cudaSuccess || (!o_bf16 && !o_f32 && !lse)) return e;   // no output requested: K3 alone
     return launch_combine_seg(g, B, o_part, ml_part, meta, o_bf16, o_f32, lse, s);
   }
@@ -558,18 +562,24 @@ tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const
   auto* y_part = reinterpret_cast<float*>(base + L.y_part);
   const auto* qn = static_cast<const uint16_t*>(q_nope);
   cudaError_t e;
+  const bool tc_path = use_tc_attention(g, B) && combine_wuv_supported(g);
+  auto* plan = reinterpret_cast<int32_t*>(base + L.plan);
+  if (tc_path) {   // K3p: K3's schedule, ahead of K2 (its latency hides under K1 / K2)
+    e = launch_attn_plan(g, *cache, seq_lens, B, L.n_cta, plan, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K3p plan");
+  }
   // K2: Q'_j[b,h,:] = W^UK'_j[h] q[b,h,:]   (mu_j folded)
   e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK), qn + size_t(g.head_begin) * g.d_h,
                        long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h, R, q_lat, true, s);
   if (e != cudaSuccess) return cuda_fail(e, "K2 absorb_q");
-  if (use_tc_attention(g, B) && combine_wuv_supported(g)) {
+  if (tc_path) {
     // K3: per-shard split-K flash decoding (Eq. tpla_softmax_one_device) -> partials;
     // K4 + K5a fused: merge the partials of each (b, h) into O_j and apply W^UV'_j
     auto* o_part = reinterpret_cast<float*>(base + L.o_part);
     auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
     auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
     e = launch_decode_attn_tc(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, n_q, L.n_cta,
-                              o_part, ml_part, meta, s);
+                              plan, o_part, ml_part, meta, s);
     if (e != cudaSuccess) return cuda_fail(e, "K3 decode attention");
     e = launch_combine_wuv(g, B, n_q, o_part, ml_part, meta, static_cast<const uint16_t*>(w->W_UV), v, s);
     if (e != cudaSuccess) return cuda_fail(e, "K4+K5a combine/W_UV");
@@ -723,12 +733,15 @@ tpla_status tpla_decode_v(const tpla_config* cfg, const tpla_weights* w, const t
   auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
   auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
   const auto* qn = static_cast<const uint16_t*>(q_nope);
-  cudaError_t e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK),
+  auto* plan = reinterpret_cast<int32_t*>(base + L.plan);
+  cudaError_t e = launch_attn_plan(g, *cache, seq_lens, B, L.n_cta, plan, s);   // K3p, ahead of K2
+  if (e != cudaSuccess) return cuda_fail(e, "K3p plan");
+  e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK),
                                    qn + size_t(g.head_begin) * g.d_h, long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h,
                                    B * n_q, q_lat, true, s);
   if (e != cudaSuccess) return cuda_fail(e, "K2 absorb_q");
-  e = launch_decode_attn_tc(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, n_q, L.n_cta, o_part,
-                            ml_part, meta, s);
+  e = launch_decode_attn_tc(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, n_q, L.n_cta, plan,
+                            o_part, ml_part, meta, s);
   if (e != cudaSuccess) return cuda_fail(e, "K3 decode attention");
   e = launch_combine_wuv(g, B, n_q, o_part, ml_part, meta, static_cast<const uint16_t*>(w->W_UV), nullptr, s, v_acc,
                          (flags & TPLA_DECODE_ACCUMULATE) != 0, n_chunks);

@@ -626,7 +626,8 @@ def test_e2e_parity_ragged_combine_blocks():
 def test_e2e_parity_mu_one(dname, k, g, kind):
     """Reading R6's alternative: mu_j = 1 (the literal §4 equations, no NoPE logit scaling)."""
     e2e_case(dev(), synth.PRESETS[dname], k, g, kind, [5, 200, 333], mu=1.0)
-    e2e_case(dev(), synth.PRESETS[dname], k, g, kind, [5, 200, 333], mu=1.0, wo="shared")
+    if dname != "tiny":                 # (the group-shared path needs the tcgen05 kernels' shapes)
+        e2e_case(dev(), synth.PRESETS[dname], k, g, kind, [5, 200, 333], mu=1.0, wo="shared")
 
 
 def dup_slices_case(d, dims, k, g, S_list, *, seed=0, wo="rank"):
