@@ -213,3 +213,25 @@ def tpla_decode_exact_logits(pb: Problem, g: int):
             v = np.einsum("hl,hld->hd", O, dws[j].W_UV)
             out[b] += v.reshape(-1) @ dws[j].W_O                      # X1 A1 + X2 A2
     return out
+
+
+def gla_decode_step(pb: Problem, g: int, *, mu=None):
+    """MLA -> GLA conversion (§3.2; contrast of §4.4 P:334 and Fig. 3):
+    the latent axis is cut into g shards AND the heads into g blocks; device i keeps only the
+    diagonal block — heads block i attend to latent shard i alone (Q_{i,i}, W^VO_{i,i}), each
+    shard normalised by its own RMSNorm (the sliced RMS of the shard, i.e. the SLICED
+    rows with alpha = g), its own softmax, and O = AllReduce(Σ_i Õ_i).  The off-diagonal
+    blocks Q_{i,j}, j != i, do not contribute ("unable to access the off-diagonal head slices",
+    P:334).  mu: NoPE logit scale per shard (default 1: the GLA equations carry none).
+    Device i is the TPLA plan of rank i at (k = g, g) restricted to heads block i of g."""
+    d_c, d_r = pb.U.shape[0], pb.k_pe[0].shape[1]
+    mu = np.ones(g) if mu is None else np.asarray(mu, float)
+    ys = []
+    for i in range(g):
+        full = make_plan(g, g, pb.h_q, d_c, d_r, i)                 # latent shard i, all heads
+        h_blk = pb.h_q // g
+        plan = DevicePlan(i, i, i, i * h_blk, (i + 1) * h_blk, full.lat_begin, full.lat_end, full.row_width)
+        dw = convert_weights(pb.W_UK, pb.W_UV, pb.gamma, pb.W_O, pb.U, plan, mu[i], d_h=pb.d_h)
+        rows = device_rows(pb, plan, pb.alpha[i])
+        ys.append(decode_device(pb.q_nope, pb.q_pe, rows, dw, plan, sm_scale=pb.sm_scale))
+    return all_reduce(ys)

@@ -50,12 +50,13 @@ constexpr int kMaxCta = 256;      // persistent grid bound (<= #SMs in practice)
 constexpr int kPlanStride = 8;    // ints per CTA entry of the K3p plan
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: p <= 2^8 between max updates
 // Every kPolyEvery-th group of 4 exponentials computes 2 of them with ex2_poly2 on the FMA pipe
-// (0 = none).  Measured (tools/gpu_variants.sh): at W_lat <= 128 a 1-in-8 share takes ~3 % off K3
-// (the MUFU-bound exponential phase shrinks); at W_lat = 256 no share helps.
+// (0 = none).  Measured (tools/gpu_ab.sh, round 2): at W_lat <= 128 a 1-in-8 share (kPolyEvery 4)
+// is the best of 0 / 1-in-8 / 1-in-4 / 1-in-2 (h8 K3 63.2 vs 63.6 us at 1-in-4, 71.4 at 1-in-2: the
+// loop is bound by one warp's issue, not by the MUFU, tools/exps_rate); at W_lat = 256 none helps.
 #ifdef TPLA_POLY_EVERY
 template <int W_LAT> constexpr int kPolyEvery = TPLA_POLY_EVERY;
 #else
-template <int W_LAT> constexpr int kPolyEvery = W_LAT <= 128 ? 2 : 0;
+template <int W_LAT> constexpr int kPolyEvery = W_LAT <= 128 ? 4 : 0;
 #endif
 
 struct TcArgs {

@@ -492,3 +492,55 @@ def test_plan_partitions_exactly_once():
 def test_plan_rejects_indivisible(bad):
     with pytest.raises(ValueError):
         plan.make_plan(bad[0], bad[1], 128, 512, 64, 0)
+
+
+# ---------------------------------------------------------------- c11: TPLA == GLA with 2 h_q heads
+@pytest.mark.parametrize("g", [2, 4])
+def test_c11_tpla_is_gla_with_duplicated_heads(g):
+    """TPLA(k = g) is algebraically a GLA system whose heads are g copies of the
+    original heads (Q' stacks Q g times; every copy keeps its W^UK / W^UV / W^O): GLA device i
+    pairs head copy i with latent shard i — exactly TPLA's device i (all heads, shard i)."""
+    dims = synth.PRESETS["odd"] if g == 2 else synth.PRESETS["tiny"]
+    pb = make_problem(dims, g=g, transform="hadamard", mu=[1.0] * g)
+    dup = tpla.Problem(W_UK=np.concatenate([pb.W_UK] * g, axis=1), W_UV=np.concatenate([pb.W_UV] * g, axis=1),
+                       gamma=pb.gamma, W_O=np.concatenate([pb.W_O] * g, axis=0), U=pb.U, alpha=pb.alpha,
+                       mu=pb.mu, c_raw=pb.c_raw, k_pe=pb.k_pe, modes=pb.modes,
+                       q_nope=np.concatenate([pb.q_nope] * g, axis=1), q_pe=np.concatenate([pb.q_pe] * g, axis=1),
+                       h_q=g * pb.h_q, d_h=pb.d_h, eps=pb.eps, sm_scale=pb.sm_scale)
+    assert rel(tpla.gla_decode_step(dup, g), tpla.tpla_decode_step(pb, g, g)) < 1e-12
+
+
+def test_gla_drops_the_off_diagonal_blocks():
+    """GLA is not MLA: with the cross blocks Q_{0,1}, Q_{1,0} dropped the output is O(1)
+    off ("significant performance degradation"); but on a model whose heads block i lives
+    only in latent shard i (W^UK / W^UV zero outside the diagonal blocks, the GLA architecture
+    itself) with per-shard exact RMS rows it is exactly that model's attention (softmax over a
+    block's own shard = softmax over the full latent, whose other shard contributes nothing)."""
+    dims = synth.PRESETS["odd"]
+    g = 2
+    pb = make_problem(dims, g=g, modes="sliced")
+    assert rel(tpla.gla_decode_step(pb, g), mla_ref(pb)) > 1e-1
+    # block-diagonal model: heads block i only reads latent shard i
+    w = dims.d_c // g
+    hb = dims.h_q // g
+    for arr in (pb.W_UK, pb.W_UV):
+        for i in range(g):
+            for j in range(g):
+                if i != j:
+                    arr[j * w:(j + 1) * w, i * hb * dims.d_h:(i + 1) * hb * dims.d_h] = 0.0
+    pb.gamma = np.ones(dims.d_c)
+    # per-head reference: head h in block i attends over RMSNorm(shard i) (P:76-79) with its own W^UK rows
+    out = np.zeros((len(pb.c_raw), pb.W_O.shape[1]))
+    for b in range(len(pb.c_raw)):
+        for i in range(g):
+            c_i = pb.c_raw[b][:, i * w:(i + 1) * w]
+            chat = c_i / np.sqrt(np.sum(c_i * c_i, axis=1) / w + pb.eps)[:, None]
+            for h in range(i * hb, (i + 1) * hb):
+                cols = slice(h * dims.d_h, (h + 1) * dims.d_h)
+                k = chat @ pb.W_UK[i * w:(i + 1) * w, cols]
+                v = chat @ pb.W_UV[i * w:(i + 1) * w, cols]
+                s = (k @ pb.q_nope[b, h] + pb.k_pe[b] @ pb.q_pe[b, h]) * pb.sm_scale
+                p = np.exp(s - s.max())
+                p /= p.sum()
+                out[b] += (p @ v) @ pb.W_O[cols]
+    assert rel(tpla.gla_decode_step(pb, g), out) < 1e-12

@@ -5,6 +5,7 @@ product path):
   TPLA (norm only)     sliced RMSNorm, exact softmax (partial logits summed before it)
   TPLA (softmax only)  exact RMSNorm, per-shard softmax
   TPLA                 sliced RMSNorm and per-shard softmax (mu = alpha, and mu = 1)
+  GLA                  MLA -> GLA conversion: heads block i sees latent shard i only
   x  U in {identity ("Original"), Hadamard, PCA},  g = 2
 
 Error = per-row ||o - o_MLA||_inf / ||o_MLA||_inf against absorbed MLA (g = 1, exact), median
@@ -26,7 +27,7 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 from oracle import mla, numerics, reparam, tpla  # noqa: E402
 
-MODES = ["norm only", "softmax only", "TPLA (mu=alpha)", "TPLA (mu=1)"]
+MODES = ["norm only", "softmax only", "TPLA (mu=alpha)", "TPLA (mu=1)", "GLA"]
 BASES = ["identity", "hadamard", "pca"]
 
 
@@ -71,6 +72,7 @@ def run(heads=16, seq=256, batch=4, g=2, natural_basis=False, seed=3):
             "softmax only": tpla.tpla_decode_step(problem(dims, U, alpha, alpha, c_raw, k_pe, q, qpe, ex), g, g),
             "TPLA (mu=alpha)": tpla.tpla_decode_step(problem(dims, U, alpha, alpha, c_raw, k_pe, q, qpe, sl), g, g),
             "TPLA (mu=1)": tpla.tpla_decode_step(problem(dims, U, alpha, np.ones(g), c_raw, k_pe, q, qpe, sl), g, g),
+            "GLA": tpla.gla_decode_step(problem(dims, U, alpha, np.ones(g), c_raw, k_pe, q, qpe, sl), g),
         }
         for m, o in outs.items():
             e = np.max(np.abs(o - o_mla), axis=1) / np.max(np.abs(o_mla), axis=1)
