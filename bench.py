@@ -84,6 +84,9 @@ def parse():
                    help="up-projection: 'rank' = every rank multiplies its own v_j by its W^O rows (P:139-141); "
                         "'shared' = the g ranks of a head block sum v first and read W^O once, reduce-scattered "
                         "across processes (SURVEY f2(ii)); auto = shared when g > 1")
+    p.add_argument("--no-rank-streams", action="store_true",
+                   help="issue the co-located ranks of a latent group serially on one stream (default: one stream "
+                        "per rank, separate v accumulators summed in tpla_project_out_sum)")
     p.add_argument("--profile-region", action="store_true",
                    help="cudaProfilerStart/Stop around the timed region (for ncu --profile-from-start off)")
     return p.parse_args()
@@ -432,26 +435,51 @@ def main():
     by_id = {rk.rank: rk for rk in ranks}
     v_acc = [torch.zeros(by_id[grp.local_ranks[0]].v_acc_shape(B * nq, grp.n_chunks), dtype=torch.float32, device=dev)
              for grp in groups]
+    # A latent group held entirely by this process (all N = 1 runs): each rank's K1 + decode_v on its own
+    # stream into its own accumulator (the ranks are independent devices in the deployment),
+    # summed in rank order by tpla_project_out_sum.  Groups spanning processes keep the in-place sum
+    # that the reduce-scatter needs.
+    par = [wo == "shared" and not args.no_rank_streams and gcomms.get(grp.procs) is None and len(grp.local_ranks) > 1
+           for grp in groups]
+    v_sep = [[torch.zeros_like(v_acc[gi]) for _ in grp.local_ranks] if par[gi] else None
+             for gi, grp in enumerate(groups)]
+    rank_streams = {r: torch.cuda.Stream(device=dev) for gi, grp in enumerate(groups) if par[gi] for r in grp.local_ranks}
     stream = torch.cuda.current_stream()
 
-    def step(i, ck=None, kp=None, q=None, qq=None, o=None):
+    def step(i, ck=None, kp=None, q=None, qq=None, o=None, serial=False):
         ck = new_ck[i % NP] if ck is None else ck
         kp = new_kp[i % NP] if kp is None else kp
         q = qn[i % NP] if q is None else q
         qq = qp[i % NP] if qq is None else qq
         o = out if o is None else o
-        for rk in ranks:
-            rk.append(ck, kp, seq_idx, pos_new, abi.RMS_SLICED)
         if wo == "shared":
-            for grp, va in zip(groups, v_acc):
-                for j, r in enumerate(grp.local_ranks):
-                    by_id[r].decode_v(q, qq, seq_lens, va, n_chunks=grp.n_chunks, accumulate=j > 0)
+            main = torch.cuda.current_stream()
+            for gi, (grp, va) in enumerate(zip(groups, v_acc)):
+                if par[gi] and not serial:                 # one stream per co-located rank
+                    for j, r in enumerate(grp.local_ranks):
+                        st = rank_streams[r]
+                        st.wait_stream(main)
+                        with torch.cuda.stream(st):
+                            by_id[r].append(ck, kp, seq_idx, pos_new, abi.RMS_SLICED)
+                            by_id[r].decode_v(q, qq, seq_lens, v_sep[gi][j], n_chunks=grp.n_chunks)
+                    for r in grp.local_ranks:
+                        main.wait_stream(rank_streams[r])
+                else:
+                    for j, r in enumerate(grp.local_ranks):
+                        by_id[r].append(ck, kp, seq_idx, pos_new, abi.RMS_SLICED)
+                        by_id[r].decode_v(q, qq, seq_lens, va, n_chunks=grp.n_chunks, accumulate=j > 0)
             for gi, (grp, va) in enumerate(zip(groups, v_acc)):
                 last = gi == len(groups) - 1
-                by_id[grp.local_ranks[0]].project_out(va, y, o if last else None, chunk=grp.chunk, accumulate=gi > 0,
-                                                      group_comm=gcomms.get(grp.procs),
-                                                      comm=comm if last else None)
+                rk0 = by_id[grp.local_ranks[0]]
+                if par[gi] and not serial:
+                    rk0.project_out_sum(v_sep[gi], y, o if last else None, chunk=grp.chunk, accumulate=gi > 0,
+                                        comm=comm if last else None)
+                else:
+                    rk0.project_out(va, y, o if last else None, chunk=grp.chunk, accumulate=gi > 0,
+                                    group_comm=gcomms.get(grp.procs), comm=comm if last else None)
             return
+        for rk in ranks:
+            rk.append(ck, kp, seq_idx, pos_new, abi.RMS_SLICED)
         for j, rk in enumerate(ranks):
             last = j == len(ranks) - 1
             if nq == 1:
@@ -494,7 +522,7 @@ def main():
         graph_all = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph_all, capture_error_mode="relaxed"):
             for i in range(args.steps):
-                step(i)
+                step(i, serial=True)                     # (one stream: per-kernel durations stay defined)
         abi.tpla_profile_enable(False)
         # the event nodes add gaps between kernels, so these durations are upper bounds
         graph_all.replay()
@@ -720,17 +748,19 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_step, "us_per_layer": ms_step * 1e3,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic", "impl": "tpla", "config": config_of(wl, N, k, g),
-                "up_projection": ("shared: the latent group's v_j summed first (co-located ranks in place; across "
+                "up_projection": ("shared: the latent group's v_j summed first (co-located ranks: one stream per rank "
+                                  "into separate accumulators, summed in rank order by tpla_project_out_sum; across "
                                   "GPUs a reduce-scatter over column chunks), W^O read once per head block "
                                   "(SURVEY f2(ii); Σ_j v_j W^O_i = (Σ_j v_j) W^O_i, P:363)" if wo == "shared" else
                                   "rank: every rank multiplies its own v_j by its W^O rows (P:139-141)"),
                 "roofline": roofline, "headline": headline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "gpu_launches_per_step": launches / args.steps, "clocks": clk, "clocks_sustained": clocks_sust,
                 "kernels": kernels,
-                "cuda_graph": graph is not None,
+                "cuda_graph": graph is not None, "rank_streams": any(par),
                 "kernel_timing": ("library CUDA events (on the launching stream) captured as graph event nodes "
                                   "around every kernel of the K timed steps, replayed right after the timed "
-                                  "replay (the nodes add small gaps: durations are upper bounds); "
+                                  "replay, with the co-located ranks on ONE stream (the timed graph overlaps them "
+                                  "on per-rank streams; the nodes add small gaps: durations are upper bounds); "
                                   "roofline.isolated_avg_launch_us: a graph of the K3 launches alone"
                                   if graph is not None else "library CUDA events inside the timed region"),
                 "hbm_gbs_per_gpu_k3": gbs, "kv_bytes_per_gpu_per_step": bytes_k3 * len(ranks)}

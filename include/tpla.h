@@ -255,6 +255,15 @@ tpla_status tpla_decode_v(const tpla_config* cfg, const tpla_weights* w, const t
 tpla_status tpla_project_out(const tpla_config* cfg, const tpla_weights* w, float* v_acc, int32_t R, int32_t n_chunks,
                              int32_t chunk, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,
                              tpla_comm* group_comm, tpla_comm* comm, void* stream);
+/* tpla_project_out_sum: tpla_project_out for a latent group whose g ranks live in THIS process and
+ * wrote SEPARATE accumulators (tpla_decode_v without TPLA_DECODE_ACCUMULATE, each on its own
+ * stream, so their attention runs concurrently): v = bf16(Σ_i v_list[i] chunk), summed in list order
+ * (deterministic), then as tpla_project_out without group_comm.  v_list: n_v (1..16) device pointers
+ * of the same [n_chunks][R][K / n_chunks] fp32 layout.  The sum Σ_j v_j W^O = (Σ_j v_j) W^O is the
+ * group-shared up-projection.  Errors as tpla_project_out. */
+tpla_status tpla_project_out_sum(const tpla_config* cfg, const tpla_weights* w, const float* const* v_list, int32_t n_v,
+                                 int32_t R, int32_t n_chunks, int32_t chunk, void* ws, size_t ws_bytes, float* y,
+                                 void* out, int32_t flags, tpla_comm* comm, void* stream);
 tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
                             const void* q_nope, const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t n_q,
                             int32_t max_seq_len, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,

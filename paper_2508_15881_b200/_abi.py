@@ -87,6 +87,8 @@ _SIGS = {
                        _P, _S, _P, _I, _I, _P], _I),
     "tpla_project_out": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), _P, _I, _I, _I, _P, _S, _P, _P, _I, _P,
                           _P, _P], _I),
+    "tpla_project_out_sum": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), _P, _I, _I, _I, _I, _P, _S, _P, _P, _I,
+                              _P, _P], _I),
     "tpla_decode_mtp": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _P, _I, _I,
                          _I, _P, _S, _P, _P, _I, _P, _P], _I),
     "tpla_decode_attention": ([C.POINTER(tpla_config), C.POINTER(tpla_cache), _P, _P, _P, _I, _I, _P, _S, _P, _P,
@@ -242,6 +244,14 @@ def tpla_project_out(cfg, w, v_acc, R, n_chunks, chunk, ws, ws_bytes, y, out=Non
                      stream=0):
     _check(_lib.tpla_project_out(C.byref(cfg), C.byref(w), _ptr(v_acc), R, n_chunks, chunk, _ptr(ws), ws_bytes, _ptr(y),
                                  _ptr(out), flags, group_comm, comm, _ptr(stream)), "tpla_project_out")
+
+
+def tpla_project_out_sum(cfg, w, v_list, R, n_chunks, chunk, ws, ws_bytes, y, out=None, flags=0, comm=None, stream=0):
+    """v_list: the co-located group's accumulators (tensors), summed in list order before W^O."""
+    arr = (C.c_void_p * len(v_list))(*[_ptr(v) for v in v_list])
+    _check(_lib.tpla_project_out_sum(C.byref(cfg), C.byref(w), C.cast(arr, C.c_void_p), len(v_list), R, n_chunks, chunk,
+                                     _ptr(ws), ws_bytes, _ptr(y), _ptr(out), flags, comm, _ptr(stream)),
+           "tpla_project_out_sum")
 
 
 def tpla_decode_attention(cfg, cache, q_lat, q_pe, seq_lens, B, max_seq_len, ws, ws_bytes, O, lse=None, stream=0):

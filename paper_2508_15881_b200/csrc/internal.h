@@ -127,5 +127,9 @@ cudaError_t launch_reduce_slices(const float* y_part, int kslices, int B, int N,
                                  cudaStream_t s);
 
 cudaError_t launch_cast_bf16(const float* y, long n, uint16_t* out, cudaStream_t s, const char* name = "C1_cast_bf16");
+// out = bf16(Σ_i src[i]) over n elements (n % 4 == 0), the sources added in list order (n_src <= 16)
+constexpr int kMaxSumSrc = 16;
+cudaError_t launch_sum_cast_bf16(const float* const* src, int n_src, long n, uint16_t* out, cudaStream_t s,
+                                 const char* name = "K5_v_sum_cast");
 
 }  // namespace tpla

@@ -183,7 +183,37 @@ __global__ void cast_kernel(const float* __restrict__ y, long n, uint16_t* __res
   *reinterpret_cast<uint2*>(out + i) = o;
 }
 
+struct SumSrc {
+  const float* p[kMaxSumSrc];
+};
+
+__global__ void sum_cast_kernel(SumSrc src, int n_src, long n, uint16_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  long i = (blockIdx.x * (long)blockDim.x + threadIdx.x) * 4;
+  if (i >= n) return;
+  float4 v = *reinterpret_cast<const float4*>(src.p[0] + i);
+  for (int k = 1; k < n_src; ++k) {          // fixed order: deterministic
+    const float4 u = *reinterpret_cast<const float4*>(src.p[k] + i);
+    v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+  }
+  uint2 o;
+  o.x = pack_bf16(v.x, v.y);
+  o.y = pack_bf16(v.z, v.w);
+  *reinterpret_cast<uint2*>(out + i) = o;
+}
+
 }  // namespace
+
+cudaError_t launch_sum_cast_bf16(const float* const* src, int n_src, long n, uint16_t* out, cudaStream_t s,
+                                 const char* name) {
+  if (n_src < 1 || n_src > kMaxSumSrc) return cudaErrorInvalidValue;
+  SumSrc a{};
+  for (int k = 0; k < n_src; ++k) a.p[k] = src[k];
+  int blocks = (int)((n / 4 + 255) / 256);
+  KernelScope ks(name, s);
+  return launch_k(sum_cast_kernel, blocks, 256, 0, s, a, n_src, n, out);
+}
 
 cudaError_t launch_head_gemv(const char* name, const uint16_t* W, const uint16_t* x, long x_batch_stride, int H,
                              int R, int C, int B, uint16_t* out_bf16, bool inputs_from_host, cudaStream_t s) {

@@ -749,21 +749,24 @@ tpla_status tpla_decode_v(const tpla_config* cfg, const tpla_weights* w, const t
   return ok();
 }
 
-tpla_status tpla_project_out(const tpla_config* cfg, const tpla_weights* w, float* v_acc, int32_t R, int32_t n_chunks,
-                             int32_t chunk, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,
-                             tpla_comm* group_comm, tpla_comm* comm, void* stream) {
+static tpla_status project_out_common(const tpla_config* cfg, const tpla_weights* w, float* const* v_list, int32_t n_v,
+                                      int32_t R, int32_t n_chunks, int32_t chunk, void* ws, size_t ws_bytes, float* y,
+                                      void* out, int32_t flags, tpla_comm* group_comm, tpla_comm* comm, void* stream) {
   Geom g{};
   tpla_status st = make_geom(cfg, &g);
   if (st) return st;
   if (!w || !w->W_O) return fail(TPLA_ERR_INVALID_ARG, "NULL weights");
-  if (!v_acc || !ws || !y) return fail(TPLA_ERR_INVALID_ARG, "NULL v_acc/ws/y");
-  if (!aligned16(v_acc) || !aligned16(ws) || !aligned16(y) || (out && !aligned16(out)))
-    return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
+  if (!v_list || n_v < 1 || n_v > kMaxSumSrc) return fail(TPLA_ERR_INVALID_ARG, "n_v=%d outside [1, %d]", n_v, kMaxSumSrc);
+  for (int i = 0; i < n_v; ++i)
+    if (!v_list[i] || !aligned16(v_list[i])) return fail(TPLA_ERR_INVALID_ARG, "v_acc %d NULL or misaligned", i);
+  if (!ws || !y) return fail(TPLA_ERR_INVALID_ARG, "NULL ws/y");
+  if (!aligned16(ws) || !aligned16(y) || (out && !aligned16(out))) return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
   const int K = g.h_loc * g.d_h;
   if (R < 1 || n_chunks < 1 || chunk < 0 || chunk >= n_chunks)
     return fail(TPLA_ERR_INVALID_ARG, "R=%d, chunk %d of %d", R, chunk, n_chunks);
   if (K % (64 * n_chunks))
     return fail(TPLA_ERR_DIVISIBILITY, "n_chunks=%d: 64*n_chunks must divide H_loc*d_h=%d", n_chunks, K);
+  if (group_comm && n_v != 1) return fail(TPLA_ERR_INVALID_ARG, "a reduce-scattered group takes one accumulator");
   if (group_comm && (group_comm->world != n_chunks || group_comm->rank != chunk))
     return fail(TPLA_ERR_INVALID_ARG, "group communicator (rank %d of %d) must be chunk %d of %d", group_comm->rank,
                 group_comm->world, chunk, n_chunks);
@@ -778,13 +781,17 @@ tpla_status tpla_project_out(const tpla_config* cfg, const tpla_weights* w, floa
   if (ws_bytes < v_bytes + part_bytes)
     return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, v_bytes + part_bytes);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  float* v_mine = v_acc + size_t(chunk) * R * kc;                  // chunk c: [R, kc] contiguous
+  const float* v_mine[kMaxSumSrc];
+  for (int i = 0; i < n_v; ++i) v_mine[i] = v_list[i] + size_t(chunk) * R * kc;   // chunk c: [R, kc] contiguous
   if (group_comm && n_chunks > 1) {                                // Σ over the group, chunk c to its rank
-    ncclResult_t r = g_nccl.ReduceScatter(v_acc, v_mine, size_t(R) * kc, ncclFloat32, ncclSum, group_comm->comm, s);
+    ncclResult_t r = g_nccl.ReduceScatter(v_list[0], v_list[0] + size_t(chunk) * R * kc, size_t(R) * kc, ncclFloat32,
+                                          ncclSum, group_comm->comm, s);
     if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclReduceScatter: %s", g_nccl.GetErrorString(r));
   }
   auto* v16 = static_cast<uint16_t*>(ws);
-  cudaError_t e = launch_cast_bf16(v_mine, long(R) * kc, v16, s, "K5_v_cast");           // v = bf16(Σ_j v_j), this slice
+  // v = bf16(Σ_j v_j), this slice (one source: the group sum is already in place)
+  cudaError_t e = n_v == 1 ? launch_cast_bf16(v_mine[0], long(R) * kc, v16, s, "K5_v_cast")
+                           : launch_sum_cast_bf16(v_mine, n_v, long(R) * kc, v16, s);
   if (e != cudaSuccess) return cuda_fail(e, "v cast");
   uint16_t* out16 = comm ? nullptr : static_cast<uint16_t*>(out);
   e = run_wo_tc(static_cast<const uint16_t*>(w->W_O), v16, g.D, K, R, static_cast<char*>(ws) + v_bytes, y,
@@ -799,6 +806,23 @@ tpla_status tpla_project_out(const tpla_config* cfg, const tpla_weights* w, floa
     }
   }
   return ok();
+}
+
+tpla_status tpla_project_out(const tpla_config* cfg, const tpla_weights* w, float* v_acc, int32_t R, int32_t n_chunks,
+                             int32_t chunk, void* ws, size_t ws_bytes, float* y, void* out, int32_t flags,
+                             tpla_comm* group_comm, tpla_comm* comm, void* stream) {
+  float* const list[1] = {v_acc};
+  return project_out_common(cfg, w, list, 1, R, n_chunks, chunk, ws, ws_bytes, y, out, flags, group_comm, comm, stream);
+}
+
+tpla_status tpla_project_out_sum(const tpla_config* cfg, const tpla_weights* w, const float* const* v_list, int32_t n_v,
+                                 int32_t R, int32_t n_chunks, int32_t chunk, void* ws, size_t ws_bytes, float* y,
+                                 void* out, int32_t flags, tpla_comm* comm, void* stream) {
+  if (!v_list) return fail(TPLA_ERR_INVALID_ARG, "NULL v_list");
+  float* list[kMaxSumSrc];
+  if (n_v < 1 || n_v > kMaxSumSrc) return fail(TPLA_ERR_INVALID_ARG, "n_v=%d outside [1, %d]", n_v, kMaxSumSrc);
+  for (int i = 0; i < n_v; ++i) list[i] = const_cast<float*>(v_list[i]);
+  return project_out_common(cfg, w, list, n_v, R, n_chunks, chunk, ws, ws_bytes, y, out, flags, nullptr, comm, stream);
 }
 
 tpla_status tpla_decode_attention(const tpla_config* cfg, const tpla_cache* cache, const void* q_lat,

@@ -196,6 +196,13 @@ class TplaRank:
         abi.tpla_project_out(self.cfg, self.weights, v_acc, R, n_chunks, chunk, self.ws, self.ws_bytes, y, out,
                              abi.DECODE_ACCUMULATE if accumulate else 0, group_comm, comm, stream_ptr(stream))
 
+    def project_out_sum(self, v_list, y, out=None, *, chunk=0, accumulate=False, comm=None, stream=None):
+        """y (+)= bf16(Σ_i v_list[i][chunk]) W^O[chunk's rows] [, all-reduce]: a co-located group whose ranks
+        wrote separate accumulators (decode_v without accumulate, e.g. on separate streams)."""
+        n_chunks, R = int(v_list[0].shape[0]), int(v_list[0].shape[1])
+        abi.tpla_project_out_sum(self.cfg, self.weights, list(v_list), R, n_chunks, chunk, self.ws, self.ws_bytes, y, out,
+                                 abi.DECODE_ACCUMULATE if accumulate else 0, comm, stream_ptr(stream))
+
     def decode_attention(self, q_lat, q_pe, seq_lens, O, lse=None, *, B: int | None = None, stream=None):
         B = int(q_lat.shape[0]) if B is None else B
         abi.tpla_decode_attention(self.cfg, self.cache, q_lat, q_pe, seq_lens, B, self.max_seq_len, self.ws,

@@ -173,6 +173,12 @@ def test_project_out_host_checks():
         with pytest.raises(abi.TplaError) as ei:
             abi.tpla_project_out(c, w, 1 << 20, 4, n_chunks, chunk, 1 << 20, 1 << 30, 1 << 20)
         assert ei.value.status == status
+    # the co-located sum: 1..16 accumulators, each non-NULL and 16-byte aligned
+    for v_list, status in [([], abi.ERR_INVALID_ARG), ([1 << 20] * 17, abi.ERR_INVALID_ARG),
+                           ([1 << 20, (1 << 20) + 4], abi.ERR_INVALID_ARG), ([1 << 20, 0], abi.ERR_INVALID_ARG)]:
+        with pytest.raises(abi.TplaError) as ei:
+            abi.tpla_project_out_sum(c, w, v_list, 4, 1, 0, 1 << 20, 1 << 30, 1 << 20)
+        assert ei.value.status == status
     assert abi.tpla_launch_count() == n_before
 
 
