@@ -234,6 +234,40 @@ tpla_status tpla_prefill_attention(const tpla_config* cfg, const tpla_weights* w
                                    const void* q_nope, const void* q_pe, int32_t seq, int32_t L, void* ws,
                                    size_t ws_bytes, float* y, void* out, int32_t flags, tpla_comm* comm, void* stream);
 
+/* MLA prefill in its NON-absorbed form (PD separation P:421):
+ * prefill is compute-bound, so it runs as MLA with the heads split over the k prefill devices and
+ * the latent unsliced (cfg: g = 1; rank r holds heads [r·h_q/k, (r+1)·h_q/k)), on keys and values
+ * up-projected per head (head dimension d_h + d_r = 192 for QK, d_h = 128 for PV, against 576 / 512
+ * for the absorbed decode form):  ĉ = RMSNorm(c^KV) with the full RMS (γ lives in the
+ * weights), k_h = ĉ W^UK_h, v_h = ĉ W^UV_h, s = sm_scale (q_h k_hᵀ + q^PE_h k^PEᵀ) causal, O_h =
+ * softmax(s) v_h (Eq. isolate_rope), y = concat_h O_h · W^O[rows of the heads]
+ * (+ all-reduce over comm).  The decode cache rows of the prompt are written separately by
+ * tpla_prefill_mla (EXACT rows in the TPLA basis), which TPLA decode then reads.
+ *   tpla_prefill_weights: per device, bf16 blocked [N/128][K/64][128][64] (K-major rows, rows past
+ *     N zero): W_UK / W_UV with N = H·d_h output features (h-major), K = d_c latent rows
+ *     (W_γ W^UK[:, heads], original basis); W_O with N = D, K = H·d_h (W^O[head rows]ᵀ).
+ *   tpla_convert_prefill_weights: host bf16 W_UK, W_UV [d_c, h_q·d_h], gamma [d_c], W_O [h_q·d_h, D]
+ *     (fp64 on the host, bf16 RNE) into caller-allocated buffers of tpla_prefill_weights_bytes.
+ *   tpla_prefill_mla_forward: c_kv [L, d_c] raw pre-norm latents, k_pe [L, d_r] post-RoPE,
+ *     q_nope [L, h_q, d_h], q_pe [L, h_q, d_r] (all heads; the device takes its block), device bf16;
+ *     y [L, D] fp32 (= or += with TPLA_DECODE_ACCUMULATE); out [L, D] bf16 or NULL; ws:
+ *     tpla_prefill_mla_workspace_bytes(cfg, L).  Needs g = 1, d_h = 128, d_r = 64, 64 | d_c,
+ *     64 | h_q·d_h / k (else TPLA_ERR_UNSUPPORTED).  Errors as tpla_decode. */
+typedef struct tpla_prefill_weights {
+  void* W_UK;
+  void* W_UV;
+  void* W_O;
+} tpla_prefill_weights;
+tpla_status tpla_prefill_weights_bytes(const tpla_config* cfg, size_t* W_UK, size_t* W_UV, size_t* W_O);
+tpla_status tpla_convert_prefill_weights(const tpla_config* cfg, const uint16_t* W_UK, const uint16_t* W_UV,
+                                         const uint16_t* gamma, const uint16_t* W_O, tpla_prefill_weights* out,
+                                         void* stream);
+tpla_status tpla_prefill_mla_workspace_bytes(const tpla_config* cfg, int32_t L, size_t* bytes);
+tpla_status tpla_prefill_mla_forward(const tpla_config* cfg, const tpla_prefill_weights* w, const void* c_kv,
+                                     const void* k_pe, const void* q_nope, const void* q_pe, int32_t L, void* ws,
+                                     size_t ws_bytes, float* y, void* out, int32_t flags, tpla_comm* comm,
+                                     void* stream);
+
 /* Up-projection shared by a latent group.  The g devices j of head block i hold
  * the same W^O rows, so Õ_i = Σ_j v_j W^O_i = (Σ_j v_j) W^O_i: the group may sum its
  * v_j = O_j W^UV'_j first and read W^O once instead of g times.  Co-located devices add into one v_acc;

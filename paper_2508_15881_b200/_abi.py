@@ -53,6 +53,10 @@ class tpla_weights(C.Structure):
                 ("xform_kind", C.c_int32), ("alpha_j", C.c_float), ("mu_j", C.c_float)]
 
 
+class tpla_prefill_weights(C.Structure):
+    _fields_ = [("W_UK", C.c_void_p), ("W_UV", C.c_void_p), ("W_O", C.c_void_p)]
+
+
 class tpla_cache(C.Structure):
     _fields_ = [("base", C.c_void_p), ("block_table", C.c_void_p), ("num_pages", C.c_int64),
                 ("page_size", C.c_int32), ("max_pages_per_seq", C.c_int32), ("row_stride", C.c_int32),
@@ -93,6 +97,12 @@ _SIGS = {
                          _I, _P, _S, _P, _P, _I, _P, _P], _I),
     "tpla_decode_attention": ([C.POINTER(tpla_config), C.POINTER(tpla_cache), _P, _P, _P, _I, _I, _P, _S, _P, _P,
                                _P], _I),
+    "tpla_prefill_weights_bytes": ([C.POINTER(tpla_config), C.POINTER(_S), C.POINTER(_S), C.POINTER(_S)], _I),
+    "tpla_convert_prefill_weights": ([C.POINTER(tpla_config), _P, _P, _P, _P, C.POINTER(tpla_prefill_weights), _P],
+                                     _I),
+    "tpla_prefill_mla_workspace_bytes": ([C.POINTER(tpla_config), _I, C.POINTER(_S)], _I),
+    "tpla_prefill_mla_forward": ([C.POINTER(tpla_config), C.POINTER(tpla_prefill_weights), _P, _P, _P, _P, _I, _P, _S,
+                                  _P, _P, _I, _P, _P], _I),
     "tpla_comm_unique_id": ([_P], _I),
     "tpla_comm_init": ([C.POINTER(_P), _P, _I, _I], _I),
     "tpla_comm_destroy": ([_P], _I),
@@ -252,6 +262,32 @@ def tpla_project_out_sum(cfg, w, v_list, R, n_chunks, chunk, ws, ws_bytes, y, ou
     _check(_lib.tpla_project_out_sum(C.byref(cfg), C.byref(w), C.cast(arr, C.c_void_p), len(v_list), R, n_chunks, chunk,
                                      _ptr(ws), ws_bytes, _ptr(y), _ptr(out), flags, comm, _ptr(stream)),
            "tpla_project_out_sum")
+
+
+def tpla_prefill_weights_bytes(cfg: tpla_config):
+    a, b, c = _S(), _S(), _S()
+    _check(_lib.tpla_prefill_weights_bytes(C.byref(cfg), C.byref(a), C.byref(b), C.byref(c)),
+           "tpla_prefill_weights_bytes")
+    return a.value, b.value, c.value
+
+
+def tpla_convert_prefill_weights(cfg, W_UK, W_UV, gamma, W_O, out: tpla_prefill_weights, stream=0):
+    arrs = [np.ascontiguousarray(x, np.uint16) for x in (W_UK, W_UV, gamma, W_O)]
+    _check(_lib.tpla_convert_prefill_weights(C.byref(cfg), *[_ptr(x) for x in arrs], C.byref(out), _ptr(stream)),
+           "tpla_convert_prefill_weights")
+
+
+def tpla_prefill_mla_workspace_bytes(cfg: tpla_config, L: int) -> int:
+    n = _S()
+    _check(_lib.tpla_prefill_mla_workspace_bytes(C.byref(cfg), L, C.byref(n)), "tpla_prefill_mla_workspace_bytes")
+    return n.value
+
+
+def tpla_prefill_mla_forward(cfg, w: tpla_prefill_weights, c_kv, k_pe, q_nope, q_pe, L, ws, ws_bytes, y, out=None,
+                             flags=0, comm=None, stream=0):
+    _check(_lib.tpla_prefill_mla_forward(C.byref(cfg), C.byref(w), _ptr(c_kv), _ptr(k_pe), _ptr(q_nope), _ptr(q_pe), L,
+                                         _ptr(ws), ws_bytes, _ptr(y), _ptr(out), flags, comm, _ptr(stream)),
+           "tpla_prefill_mla_forward")
 
 
 def tpla_decode_attention(cfg, cache, q_lat, q_pe, seq_lens, B, max_seq_len, ws, ws_bytes, O, lse=None, stream=0):

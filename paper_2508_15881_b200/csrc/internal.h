@@ -115,8 +115,19 @@ size_t wo_tc_part_bytes(int N, int K, int B);
 // out_bf16 (optional): also write bf16(y) (the step's output when no all-reduce follows)
 // [k_begin, k_begin + k_len): a 64-multiple slice of W^O's K rows (k_len 0 = all); v is then [B, k_len],
 // the slice's columns only (a rank projecting its share of a v summed over the latent group)
+// v_ld: v's row stride in elements (0: k_len, dense rows)
 cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, void* part_ws, float* y,
-                         bool accumulate, uint16_t* out_bf16, cudaStream_t s, int k_begin = 0, int k_len = 0);
+                         bool accumulate, uint16_t* out_bf16, cudaStream_t s, int k_begin = 0, int k_len = 0,
+                         long v_ld = 0);
+
+// K8: causal prefill attention, non-absorbed MLA (k7_prefill_fa.cu).  q_nope [L, h_q*128] and q_pe
+// [L, h_q*64] hold all heads (this device's head 0 is q_head0); K, V, O [L, H*128] bf16; k_pe rows of
+// 64 with row stride kpe_ld elements.
+cudaError_t launch_attn_fwd_causal(const uint16_t* q_nope, const uint16_t* q_pe, int h_q, int q_head0,
+                                   const uint16_t* K, const uint16_t* V, int H, const uint16_t* k_pe, long kpe_ld,
+                                   int L, float sm_scale, uint16_t* O, cudaStream_t s);
+// ĉ = c / sqrt(|c|^2 / d_c + eps) per row (the full RMS; gamma lives in the up-projection weights)
+cudaError_t launch_prefill_rmsnorm(const uint16_t* c_kv, int L, int d_c, float eps, uint16_t* c_hat, cudaStream_t s);
 
 // K6: page-table rows + lengths of the prefill pseudo-sequences (k6_prefill.cu)
 cudaError_t launch_prefix_table(const int32_t* block_table, int seq, int max_pages, int n_full, int n_q, int r0,

@@ -210,11 +210,11 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-bool make_map(CUtensorMap* m, const void* base, long cols, long rows, int box_c, int box_r) {
+bool make_map(CUtensorMap* m, const void* base, long cols, long rows, int box_c, int box_r, long ld = 0) {
   EncodeFn enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
-  cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
+  cuuint64_t strides[1] = {cuuint64_t(ld > 0 ? ld : cols) * 2};
   cuuint32_t box[2] = {cuuint32_t(box_c), cuuint32_t(box_r)};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
@@ -264,13 +264,13 @@ size_t wo_tc_part_bytes(int N, int K, int B) {
 }
 
 cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, void* part_ws, float* y,
-                         bool accumulate, uint16_t* out_bf16, cudaStream_t s, int k_begin, int k_len) {
+                         bool accumulate, uint16_t* out_bf16, cudaStream_t s, int k_begin, int k_len, long v_ld) {
   if (k_len <= 0) k_len = K;
   const int n_tiles = (N + kTM - 1) / kTM;
   const int NP = B <= 32 ? 32 : B <= 64 ? 64 : B <= 128 ? 128 : 256;
   CUtensorMap mA, mB;
   // A: the blocked weights viewed as [n_tiles * k_steps * 128 rows, 64 cols]
-  if (!make_map(&mA, Wt, kBK, long(n_tiles) * (K / kBK) * kTM, kBK, kTM) || !make_map(&mB, v, k_len, B, kBK, NP))
+  if (!make_map(&mA, Wt, kBK, long(n_tiles) * (K / kBK) * kTM, kBK, kTM) || !make_map(&mB, v, k_len, B, kBK, NP, v_ld))
     return cudaErrorInvalidValue;
   GArgs a;
   a.part = static_cast<float*>(part_ws);

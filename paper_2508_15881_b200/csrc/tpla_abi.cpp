@@ -825,6 +825,162 @@ tpla_status tpla_project_out_sum(const tpla_config* cfg, const tpla_weights* w, 
   return project_out_common(cfg, w, list, n_v, R, n_chunks, chunk, ws, ws_bytes, y, out, flags, nullptr, comm, stream);
 }
 
+// ---- MLA prefill, non-absorbed: K8 ------------------------------------------------
+namespace {
+// Blocked K-major layout of a [N, K] bf16 matrix for the tcgen05 weight-stream GEMM: element (n, k)
+// at ((n / 128) * (K / 64) + k / 64) * 8192 + (n % 128) * 64 + k % 64; rows >= N zero.
+size_t blocked_elems(int N, int K) { return size_t((N + 127) / 128) * 128 * K; }
+inline size_t blocked_index(int n, int k, int K) {
+  return (size_t(n / 128) * (K / 64) + k / 64) * 8192 + size_t(n % 128) * 64 + k % 64;
+}
+struct PfGeom {
+  int H, h0, Kf;   // heads of this device, first head, H·d_h
+};
+tpla_status prefill_geom(const tpla_config* cfg, Geom* g, PfGeom* p) {
+  tpla_status st = make_geom(cfg, g);
+  if (st) return st;
+  if (g->g != 1) return fail(TPLA_ERR_UNSUPPORTED, "MLA prefill splits heads only (g = 1, P:421), got g=%d", g->g);
+  if (g->d_h != 128 || g->d_r != 64 || g->d_c % 64)
+    return fail(TPLA_ERR_UNSUPPORTED, "MLA prefill kernels need d_h=128, d_r=64, 64 | d_c (got %d, %d, %d)", g->d_h,
+                g->d_r, g->d_c);
+  p->H = g->h_loc;
+  p->h0 = g->head_begin;
+  p->Kf = g->h_loc * g->d_h;
+  if (p->Kf % 64) return fail(TPLA_ERR_UNSUPPORTED, "H*d_h=%d must be a multiple of 64", p->Kf);
+  return TPLA_OK;
+}
+struct PfWs {
+  size_t c_hat, K, V, O, y, part, total;
+};
+constexpr int kPfRows = 256;   // token rows per GEMM launch (the weight-stream GEMM's N)
+PfWs pf_ws(const Geom& g, const PfGeom& p, int L) {
+  PfWs w{};
+  size_t off = 0;
+  w.c_hat = off; off += align256(size_t(L) * g.d_c * 2);
+  w.K = off;     off += align256(size_t(L) * p.Kf * 2);
+  w.V = off;     off += align256(size_t(L) * p.Kf * 2);
+  w.O = off;     off += align256(size_t(L) * p.Kf * 2);
+  w.y = off;     off += align256(size_t(kPfRows) * std::max(p.Kf, g.D) * 4);
+  w.part = off;  off += align256(std::max(wo_tc_part_bytes(p.Kf, g.d_c, kPfRows), wo_tc_part_bytes(g.D, p.Kf, kPfRows)));
+  w.total = off;
+  return w;
+}
+}  // namespace
+
+tpla_status tpla_prefill_weights_bytes(const tpla_config* cfg, size_t* W_UK, size_t* W_UV, size_t* W_O) {
+  Geom g{};
+  PfGeom p{};
+  tpla_status st = prefill_geom(cfg, &g, &p);
+  if (st) return st;
+  if (W_UK) *W_UK = blocked_elems(p.Kf, g.d_c) * 2;
+  if (W_UV) *W_UV = blocked_elems(p.Kf, g.d_c) * 2;
+  if (W_O) *W_O = blocked_elems(g.D, p.Kf) * 2;
+  return ok();
+}
+
+tpla_status tpla_convert_prefill_weights(const tpla_config* cfg, const uint16_t* W_UK, const uint16_t* W_UV,
+                                         const uint16_t* gamma, const uint16_t* W_O, tpla_prefill_weights* out,
+                                         void* stream) {
+  Geom g{};
+  PfGeom p{};
+  tpla_status st = prefill_geom(cfg, &g, &p);
+  if (st) return st;
+  if (!W_UK || !W_UV || !gamma || !W_O || !out || !out->W_UK || !out->W_UV || !out->W_O)
+    return fail(TPLA_ERR_INVALID_ARG, "NULL argument");
+  const int d_c = g.d_c, hq_dh = g.h_q * g.d_h, D = g.D;
+  std::vector<uint16_t> uk(blocked_elems(p.Kf, d_c), 0), uv(blocked_elems(p.Kf, d_c), 0), wo(blocked_elems(D, p.Kf), 0);
+  // k = ĉ W_γ W^UK[:, heads]: row n = local feature (h·d_h + e), column k = latent l (original basis)
+  parallel_for(d_c, [&](int l) {
+    const double gm = bf16_to_double(gamma[l]);
+    for (int n = 0; n < p.Kf; ++n) {
+      const size_t src = size_t(l) * hq_dh + size_t(p.h0) * g.d_h + n;
+      uk[blocked_index(n, l, d_c)] = double_to_bf16(gm * bf16_to_double(W_UK[src]));
+      uv[blocked_index(n, l, d_c)] = double_to_bf16(gm * bf16_to_double(W_UV[src]));
+    }
+  });
+  parallel_for(p.Kf, [&](int kk) {      // y = O W^O[head rows]: row n = output d, column = local feature kk
+    const uint16_t* src = W_O + (size_t(p.h0) * g.d_h + kk) * D;
+    for (int n = 0; n < D; ++n) wo[blocked_index(n, kk, p.Kf)] = src[n];
+  });
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TPLA_CUDA(cudaMemcpyAsync(out->W_UK, uk.data(), uk.size() * 2, cudaMemcpyHostToDevice, s), "copy W_UK");
+  TPLA_CUDA(cudaMemcpyAsync(out->W_UV, uv.data(), uv.size() * 2, cudaMemcpyHostToDevice, s), "copy W_UV");
+  TPLA_CUDA(cudaMemcpyAsync(out->W_O, wo.data(), wo.size() * 2, cudaMemcpyHostToDevice, s), "copy W_O");
+  TPLA_CUDA(cudaStreamSynchronize(s), "convert sync");
+  return ok();
+}
+
+tpla_status tpla_prefill_mla_workspace_bytes(const tpla_config* cfg, int32_t L, size_t* bytes) {
+  Geom g{};
+  PfGeom p{};
+  tpla_status st = prefill_geom(cfg, &g, &p);
+  if (st) return st;
+  if (L < 1 || !bytes) return fail(TPLA_ERR_INVALID_ARG, "L=%d", L);
+  *bytes = pf_ws(g, p, L).total;
+  return ok();
+}
+
+tpla_status tpla_prefill_mla_forward(const tpla_config* cfg, const tpla_prefill_weights* w, const void* c_kv,
+                                     const void* k_pe, const void* q_nope, const void* q_pe, int32_t L, void* ws,
+                                     size_t ws_bytes, float* y, void* out, int32_t flags, tpla_comm* comm,
+                                     void* stream) {
+  Geom g{};
+  PfGeom p{};
+  tpla_status st = prefill_geom(cfg, &g, &p);
+  if (st) return st;
+  if (!w || !w->W_UK || !w->W_UV || !w->W_O) return fail(TPLA_ERR_INVALID_ARG, "NULL weights");
+  if (!c_kv || !k_pe || !q_nope || !q_pe || !ws || !y) return fail(TPLA_ERR_INVALID_ARG, "NULL input");
+  if (!aligned16(c_kv) || !aligned16(k_pe) || !aligned16(q_nope) || !aligned16(q_pe) || !aligned16(ws) || !aligned16(y) ||
+      (out && !aligned16(out)))
+    return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
+  if (L < 1) return fail(TPLA_ERR_INVALID_ARG, "L=%d", L);
+  if (comm && (g.k % comm->world))
+    return fail(TPLA_ERR_INVALID_ARG, "communicator world %d does not divide k=%d", comm->world, g.k);
+  if (comm && !load_nccl()) return fail(TPLA_ERR_NCCL, "NCCL not loadable");
+  const PfWs L_ = pf_ws(g, p, L);
+  if (ws_bytes < L_.total) return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, L_.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(ws);
+  auto* c_hat = reinterpret_cast<uint16_t*>(base + L_.c_hat);
+  auto* Kb = reinterpret_cast<uint16_t*>(base + L_.K);
+  auto* Vb = reinterpret_cast<uint16_t*>(base + L_.V);
+  auto* Ob = reinterpret_cast<uint16_t*>(base + L_.O);
+  auto* yscr = reinterpret_cast<float*>(base + L_.y);
+  void* part = base + L_.part;
+  // ĉ = RMSNorm(c) (full RMS)
+  cudaError_t e = launch_prefill_rmsnorm(static_cast<const uint16_t*>(c_kv), L, g.d_c, g.eps, c_hat, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K8 rmsnorm");
+  // k = ĉ W^UK_h, v = ĉ W^UV_h for this device's heads (tcgen05 weight-stream GEMM, 256 rows per launch;
+  // the fp32 sums land in a scratch, the bf16 copy is the product)
+  for (int r0 = 0; r0 < L; r0 += kPfRows) {
+    const int n = std::min(kPfRows, L - r0);
+    e = launch_wo_tc(static_cast<const uint16_t*>(w->W_UK), c_hat + size_t(r0) * g.d_c, p.Kf, g.d_c, n, part, yscr,
+                     false, Kb + size_t(r0) * p.Kf, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K8 k up-projection");
+    e = launch_wo_tc(static_cast<const uint16_t*>(w->W_UV), c_hat + size_t(r0) * g.d_c, p.Kf, g.d_c, n, part, yscr,
+                     false, Vb + size_t(r0) * p.Kf, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K8 v up-projection");
+  }
+  // causal attention per head (Eq. isolate_rope)
+  e = launch_attn_fwd_causal(static_cast<const uint16_t*>(q_nope), static_cast<const uint16_t*>(q_pe), g.h_q, p.h0, Kb,
+                             Vb, p.H, static_cast<const uint16_t*>(k_pe), g.d_r, L, g.sm_scale, Ob, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K8 attention");
+  // y = concat_h O_h · W^O[head rows], then the all-reduce over the head-split devices
+  const bool accumulate = (flags & TPLA_DECODE_ACCUMULATE) != 0;
+  e = run_wo_tc(static_cast<const uint16_t*>(w->W_O), Ob, g.D, p.Kf, L, part, y, accumulate,
+                comm ? nullptr : static_cast<uint16_t*>(out), s);
+  if (e != cudaSuccess) return cuda_fail(e, "K8 W^O");
+  if (comm) {
+    ncclResult_t r = g_nccl.AllReduce(y, y, size_t(L) * g.D, ncclFloat32, ncclSum, comm->comm, s);
+    if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
+    if (out) {
+      e = launch_cast_bf16(y, long(L) * g.D, static_cast<uint16_t*>(out), s);
+      if (e != cudaSuccess) return cuda_fail(e, "cast");
+    }
+  }
+  return ok();
+}
+
 tpla_status tpla_decode_attention(const tpla_config* cfg, const tpla_cache* cache, const void* q_lat,
                                   const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t max_seq_len,
                                   void* ws, size_t ws_bytes, float* O, float* lse, void* stream) {

@@ -215,3 +215,34 @@ class TplaRank:
         pages = self.block_table[b].long()[t // self.page_size]
         return bits_from_bf16(self.cache_buf[pages, t % self.page_size])     # gathered on the device
 
+
+
+class PrefillRank:
+    """One device of the PD-separated MLA prefill: heads split over k devices,
+    latent unsliced (g = 1), keys / values up-projected per head (tpla_prefill_mla_forward)."""
+
+    def __init__(self, spec: LayerSpec, *, k: int, rank: int, max_len: int, device="cuda"):
+        self.spec = spec
+        self.k, self.rank = k, rank
+        self.cfg = make_config(spec, k, 1, rank)
+        self.device = torch.device(device)
+        self.max_len = max_len
+        self.ws_bytes = abi.tpla_prefill_mla_workspace_bytes(self.cfg, max_len)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.weights = None
+
+    def convert(self, W_UK, W_UV, gamma, W_O):
+        nuk, nuv, nwo = abi.tpla_prefill_weights_bytes(self.cfg)
+        self._wbufs = tuple(torch.empty(n // 2, dtype=torch.bfloat16, device=self.device) for n in (nuk, nuv, nwo))
+        w = abi.tpla_prefill_weights(*[b.data_ptr() for b in self._wbufs])
+        abi.tpla_convert_prefill_weights(self.cfg, W_UK, W_UV, gamma, W_O, w, stream_ptr())
+        self.weights = w
+        return w
+
+    def forward(self, c_kv, k_pe, q_nope, q_pe, y, out=None, *, accumulate=False, comm=None, stream=None):
+        """c_kv [L, d_c] raw latents, k_pe [L, d_r], q_nope [L, h_q, d_h], q_pe [L, h_q, d_r] (bf16, device);
+        y [L, D] fp32 (+= with accumulate), out [L, D] bf16 or None."""
+        L = int(c_kv.shape[0])
+        assert L <= self.max_len
+        abi.tpla_prefill_mla_forward(self.cfg, self.weights, c_kv, k_pe, q_nope, q_pe, L, self.ws, self.ws_bytes, y, out,
+                                     abi.DECODE_ACCUMULATE if accumulate else 0, comm, stream_ptr(stream))

@@ -191,3 +191,21 @@ def test_import_fails_loudly_without_library(tmp_path):
     code = "from paper_2508_15881_b200 import abi"
     r = subprocess.run([sys.executable, "-c", code], cwd=tmp_path, capture_output=True, text=True)
     assert r.returncode != 0 and "libtpla.so" in r.stderr
+
+
+def test_prefill_mla_forward_host_checks():
+    """the non-absorbed MLA prefill splits heads only (g = 1) and needs d_h = 128, d_r = 64."""
+    c = cfg()                                            # g = 2 -> unsupported
+    w = abi.tpla_prefill_weights(1 << 20, 1 << 20, 1 << 20)
+    n_before = abi.tpla_launch_count()
+    with pytest.raises(abi.TplaError) as ei:
+        abi.tpla_prefill_mla_forward(c, w, 1 << 20, 1 << 20, 1 << 20, 1 << 20, 64, 1 << 20, 1 << 30, 1 << 20)
+    assert ei.value.status == abi.ERR_UNSUPPORTED
+    c1 = abi.tpla_config(128, 512, 64, 128, 7168, 2, 1, 1, 1e-6, 0.07)
+    assert abi.tpla_prefill_mla_workspace_bytes(c1, 4096) > 4096 * 64 * 128 * 2 * 3
+    uk, uv, wo = abi.tpla_prefill_weights_bytes(c1)
+    assert uk == uv == 64 * 128 * 512 * 2 and wo == 7168 * 64 * 128 * 2
+    with pytest.raises(abi.TplaError) as ei:             # workspace too small
+        abi.tpla_prefill_mla_forward(c1, w, 1 << 20, 1 << 20, 1 << 20, 1 << 20, 4096, 1 << 20, 1024, 1 << 20)
+    assert ei.value.status == abi.ERR_CAPACITY
+    assert abi.tpla_launch_count() == n_before

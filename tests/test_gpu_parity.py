@@ -746,3 +746,45 @@ def test_wo_mma_baseline_reads_blocked_layout(monkeypatch):
     monkeypatch.setenv("TPLA_WO", "mma")
     e2e_case(dev(), synth.PRESETS["dsv3"], 2, 2, "hadamard", [5, 200, 333])
     e2e_case(dev(), synth.PRESETS["dsv3"], 8, 2, "identity", [64, 129])
+
+
+# ----------------------------------------------------------------------------- f1: non-absorbed MLA prefill
+def prefill_mla_forward_case(d, dims, k, L, *, sample=None, seed=0):
+    """SURVEY f1, PD separation: the prompt's causal attention as MLA with the heads split over k
+    devices and the latent unsliced, keys/values up-projected per head (K8), then W^O and the sum over
+    the devices.  Pinned to the oracle's non-absorbed MLA (oracle/mla.py, Eq. isolate_rope)
+    per prompt position t over the prefix 0..t."""
+    from paper_2508_15881_b200.runtime import PrefillRank
+    w = synth.gen_weights(dims, seed + 1)
+    q, qpe = synth.gen_queries(dims, L, seed + 2)
+    c_raw = synth.gen_raw_ckv(dims, L, seed + 3, 0)
+    k_pe = synth.gen_kpe(dims, L, seed + 3, 0)
+    y = torch.zeros((L, dims.D), dtype=torch.float32, device=d)
+    out = torch.empty((L, dims.D), dtype=torch.bfloat16, device=d)
+    args = [bf16_from_bits(x, d) for x in (c_raw, k_pe, q, qpe)]
+    for r in range(k):
+        pr = PrefillRank(spec_of(dims), k=k, rank=r, max_len=L, device=d)
+        pr.convert(w.W_UK, w.W_UV, w.gamma, w.W_O)
+        pr.forward(*args, y, out if r == k - 1 else None, accumulate=r > 0)
+    torch.cuda.synchronize()
+    got = y.cpu().numpy()
+    ts = range(L) if sample is None else sorted(set(list(range(0, L, sample)) + [L - 1, 127, 128]) & set(range(L)))
+    W = [f64(x) for x in (w.W_UK, w.W_UV, w.gamma, w.W_O)]
+    for t in ts:
+        ref = mla.mla_decode_full(f64(q[t]), f64(qpe[t]), f64(c_raw[:t + 1]), f64(k_pe[:t + 1]), *W, h_q=dims.h_q,
+                                  d_h=dims.d_h, eps=1e-6, sm_scale=dims_scale(dims))[0]
+        e = row_rel_err(got[t:t + 1], ref[None])
+        assert e <= TOL, (t, e)
+    if k == 1:
+        assert torch.equal(out, y.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("k,L", [(1, 129), (2, 300), (4, 77)])
+def test_prefill_mla_forward(k, L):
+    """Ragged query / key tiles (L % 128 != 0), two 256-row GEMM chunks, heads split 1 / 2 / 4 ways."""
+    prefill_mla_forward_case(dev(), synth.PRESETS["dsv3"], k, L, sample=7)
+
+
+def test_prefill_mla_forward_kimi_long():
+    """Kimi-K2 heads (64), a 1100-token prompt: 9 query tiles, the longest attending to 9 key tiles."""
+    prefill_mla_forward_case(dev(), synth.PRESETS["kimi"], 2, 1100, sample=97)
