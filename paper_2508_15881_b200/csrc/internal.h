@@ -126,6 +126,11 @@ cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, in
 cudaError_t launch_attn_fwd_causal(const uint16_t* q_nope, const uint16_t* q_pe, int h_q, int q_head0,
                                    const uint16_t* K, const uint16_t* V, int H, const uint16_t* k_pe, long kpe_ld,
                                    int L, float sm_scale, uint16_t* O, cudaStream_t s);
+// K9: out[t, n] = Σ_k X[t, k] Wt[n, k] for t < L (X row stride ld_x; Wt blocked like W^O): fp32 y (=, or
+// += with accumulate) and/or bf16 out, either may be null.  One CTA per [128 x 256] tile, full K.
+bool gemm_tn_supported(int N, int K);
+cudaError_t launch_gemm_tn(const uint16_t* Wt, const uint16_t* X, long ld_x, int N, int K, int L, float* y,
+                           bool accumulate, uint16_t* out, cudaStream_t s);
 // ĉ = c / sqrt(|c|^2 / d_c + eps) per row (the full RMS; gamma lives in the up-projection weights)
 cudaError_t launch_prefill_rmsnorm(const uint16_t* c_kv, int L, int d_c, float eps, uint16_t* c_hat, cudaStream_t s);
 

@@ -1,0 +1,182 @@
+// K9 — the prefill's dense GEMMs: the per-head key / value up-projections k = ĉ W^UK_h,
+// v = ĉ W^UV_h and the output projection y = concat_h O_h W^O over all L prompt rows.
+//
+//   out[t, n] = Σ_k X[t, k] · Wt[n, k]        X: [L, K] bf16 activations (row stride ld_x),
+//                                             Wt: blocked K-major weights [ceil(N/128)][K/64][128][64]
+//
+// One CTA per [256 weight rows x 256 tokens] output tile, the whole K loop: two M = 128 MMAs (the two
+// weight row tiles, swap-AB: D[128 x 256] fp32 each, the 512 TMEM columns) share each [256 x 64]
+// activation box, so a k-step moves 64 KB (two 16 KB weight blocks + the box) for 8.4 MFLOP — with one
+// row tile per CTA (48 KB for 4.2 MFLOP) the kernel was bound by the L2 -> SM operand traffic
+// (measured ~512 TFLOP/s).  TMA streams the operands through a 3-stage mbarrier ring; one thread
+// issues tcgen05.mma; the epilogue (8 warps: TMEM lane quadrant x row tile, thread = weight row)
+// writes out[t, n] token column by token column, 128 contiguous bytes per warp (fp32 y, =/+=, and/or
+// a bf16 copy).  Unlike the decode's weight-stream K5 (split-K over a huge K, a few rows), nothing is
+// split over K here: no partials, no reduce pass.  CTAs sharing a weight tile run back to back
+// (token tile fastest), so each weight block comes from HBM once and from L2 for the rest.
+//
+// Warp roles (384 threads): w0 TMA, w1 MMA, w2 TMEM allocator, w4-w11 epilogue.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace tpla {
+namespace {
+
+using namespace sm100;
+
+constexpr int kM = 128, kN = 256, kK = 64;
+constexpr int kMT = 2;                        // weight row tiles per CTA (MMA M = 128 each)
+constexpr int kWBytes = kM * 128;             // 16 KB per row tile
+constexpr int kXBytes = kN * 128;             // 32 KB
+constexpr int kStage = kMT * kWBytes + kXBytes;
+constexpr int kStages = 3;
+constexpr int kSmem = 1024 + kStages * kStage;
+
+struct G9Args {
+  float* y;           // [L, N] fp32 or null
+  uint16_t* out;      // [L, N] bf16 or null
+  int N, L, k_steps, n_tt, n_rt, accumulate;
+};
+
+__global__ void __launch_bounds__(384, 1)
+gemm_tn_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mx, G9Args a) {
+  pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[kStages], empty[kStages], acc_full;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rp = int(blockIdx.x) / a.n_tt, tt = int(blockIdx.x) % a.n_tt;   // row-tile pair, token tile
+  const int n_mt = min(kMT, a.n_rt - rp * kMT);                            // (the last pair may be single)
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mw);
+    tma_prefetch_desc(&mx);
+    for (int i = 0; i < kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(&acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<kMT * kN>(&tmem_base);
+  pdl_wait();                                   // X (and y) come from the predecessors
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tmem_base;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int ks = 0; ks < a.k_steps; ++ks) {
+        const int st = ks % kStages;
+        mbar_wait(&empty[st], ((ks / kStages) & 1) ^ 1);
+        uint8_t* dst = smem + st * kStage;
+        mbar_arrive_expect_tx(&full[st], n_mt * kWBytes + kXBytes);
+        for (int m = 0; m < n_mt; ++m)
+          tma_load_2d(dst + m * kWBytes, &mw, 0, ((rp * kMT + m) * a.k_steps + ks) * kM, &full[st], kEvictNormal);
+        tma_load_2d(dst + kMT * kWBytes, &mx, ks * kK, tt * kN, &full[st], kEvictNormal);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(kM, kN, false, false);
+    constexpr uint32_t hi_k = desc_sw128_hi(1024);
+    const uint32_t s0 = smem_addr(smem);
+    for (int ks = 0; ks < a.k_steps; ++ks) {
+      const int st = ks % kStages;
+      mbar_wait(&full[st], (ks / kStages) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t db = make_desc(s0 + st * kStage + kMT * kWBytes, 16, hi_k);
+        for (int m = 0; m < n_mt; ++m) {
+          const uint64_t da = make_desc(s0 + st * kStage + m * kWBytes, 16, hi_k);
+#pragma unroll
+          for (int kk = 0; kk < kK / 16; ++kk)
+            mma_ss(tb + m * kN, da + uint64_t(kk * 2), db + uint64_t(kk * 2), idesc, (ks == 0 && kk == 0) ? 0u : 1u);
+        }
+        mma_commit(&empty[st]);
+        if (ks + 1 == a.k_steps) mma_commit(&acc_full);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4 && (warp - 4) / 4 < n_mt) {
+    const int q4 = warp & 3, m = (warp - 4) / 4;   // TMEM lane quadrant, row tile of the pair
+    const int n = (rp * kMT + m) * kM + q4 * 32 + lane;   // weight row = output feature
+    const uint32_t lane_base = tb + m * kN + (uint32_t(q4 * 32) << 16);
+    mbar_wait(&acc_full, 0);
+    tc_fence_after();
+    const bool n_ok = n < a.N;
+#pragma unroll 1
+    for (int c0 = 0; c0 < kN; c0 += 32) {
+      uint32_t d[32];
+      tmem_ld32(lane_base + c0, d);
+      tmem_ld_wait();
+      const int t0 = tt * kN + c0;
+      if (n_ok) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int t = t0 + j;
+          if (t < a.L) {
+            float v = __uint_as_float(d[j]);
+            const long i = (long)t * a.N + n;
+            if (a.y) {
+              if (a.accumulate) v += a.y[i];
+              a.y[i] = v;
+            }
+            if (a.out) a.out[i] = f2bf(v);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<kMT * kN>(tb);
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool map2d(CUtensorMap* m, const void* base, long cols, long rows, long ld, int box_r) {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
+  cuuint32_t box[2] = {cuuint32_t(kK), cuuint32_t(box_r)};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool gemm_tn_supported(int N, int K) { return N >= 1 && K >= kK && K % kK == 0; }
+
+cudaError_t launch_gemm_tn(const uint16_t* Wt, const uint16_t* X, long ld_x, int N, int K, int L, float* y,
+                           bool accumulate, uint16_t* out, cudaStream_t s) {
+  const int n_rt = (N + kM - 1) / kM, n_tt = (L + kN - 1) / kN, n_rp = (n_rt + kMT - 1) / kMT;
+  CUtensorMap mw, mx;
+  if (!map2d(&mw, Wt, kK, long(n_rt) * (K / kK) * kM, kK, kM) || !map2d(&mx, X, K, L, ld_x, kN))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  G9Args a{y, out, N, L, K / kK, n_tt, n_rt, accumulate ? 1 : 0};
+  KernelScope ks("K9_prefill_gemm", s);
+  return launch_k(gemm_tn_kernel, n_rp * n_tt, 384, kSmem, s, mw, mx, a);
+}
+
+}  // namespace tpla

@@ -850,9 +850,8 @@ tpla_status prefill_geom(const tpla_config* cfg, Geom* g, PfGeom* p) {
   return TPLA_OK;
 }
 struct PfWs {
-  size_t c_hat, K, V, O, y, part, total;
+  size_t c_hat, K, V, O, total;
 };
-constexpr int kPfRows = 256;   // token rows per GEMM launch (the weight-stream GEMM's N)
 PfWs pf_ws(const Geom& g, const PfGeom& p, int L) {
   PfWs w{};
   size_t off = 0;
@@ -860,8 +859,6 @@ PfWs pf_ws(const Geom& g, const PfGeom& p, int L) {
   w.K = off;     off += align256(size_t(L) * p.Kf * 2);
   w.V = off;     off += align256(size_t(L) * p.Kf * 2);
   w.O = off;     off += align256(size_t(L) * p.Kf * 2);
-  w.y = off;     off += align256(size_t(kPfRows) * std::max(p.Kf, g.D) * 4);
-  w.part = off;  off += align256(std::max(wo_tc_part_bytes(p.Kf, g.d_c, kPfRows), wo_tc_part_bytes(g.D, p.Kf, kPfRows)));
   w.total = off;
   return w;
 }
@@ -945,31 +942,23 @@ tpla_status tpla_prefill_mla_forward(const tpla_config* cfg, const tpla_prefill_
   auto* Kb = reinterpret_cast<uint16_t*>(base + L_.K);
   auto* Vb = reinterpret_cast<uint16_t*>(base + L_.V);
   auto* Ob = reinterpret_cast<uint16_t*>(base + L_.O);
-  auto* yscr = reinterpret_cast<float*>(base + L_.y);
-  void* part = base + L_.part;
   // ĉ = RMSNorm(c) (full RMS)
   cudaError_t e = launch_prefill_rmsnorm(static_cast<const uint16_t*>(c_kv), L, g.d_c, g.eps, c_hat, s);
   if (e != cudaSuccess) return cuda_fail(e, "K8 rmsnorm");
-  // k = ĉ W^UK_h, v = ĉ W^UV_h for this device's heads (tcgen05 weight-stream GEMM, 256 rows per launch;
-  // the fp32 sums land in a scratch, the bf16 copy is the product)
-  for (int r0 = 0; r0 < L; r0 += kPfRows) {
-    const int n = std::min(kPfRows, L - r0);
-    e = launch_wo_tc(static_cast<const uint16_t*>(w->W_UK), c_hat + size_t(r0) * g.d_c, p.Kf, g.d_c, n, part, yscr,
-                     false, Kb + size_t(r0) * p.Kf, s);
-    if (e != cudaSuccess) return cuda_fail(e, "K8 k up-projection");
-    e = launch_wo_tc(static_cast<const uint16_t*>(w->W_UV), c_hat + size_t(r0) * g.d_c, p.Kf, g.d_c, n, part, yscr,
-                     false, Vb + size_t(r0) * p.Kf, s);
-    if (e != cudaSuccess) return cuda_fail(e, "K8 v up-projection");
-  }
+  // k = ĉ W^UK_h, v = ĉ W^UV_h for this device's heads (K9 tcgen05 GEMM, bf16 out)
+  e = launch_gemm_tn(static_cast<const uint16_t*>(w->W_UK), c_hat, g.d_c, p.Kf, g.d_c, L, nullptr, false, Kb, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K9 k up-projection");
+  e = launch_gemm_tn(static_cast<const uint16_t*>(w->W_UV), c_hat, g.d_c, p.Kf, g.d_c, L, nullptr, false, Vb, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K9 v up-projection");
   // causal attention per head (Eq. isolate_rope)
   e = launch_attn_fwd_causal(static_cast<const uint16_t*>(q_nope), static_cast<const uint16_t*>(q_pe), g.h_q, p.h0, Kb,
                              Vb, p.H, static_cast<const uint16_t*>(k_pe), g.d_r, L, g.sm_scale, Ob, s);
   if (e != cudaSuccess) return cuda_fail(e, "K8 attention");
   // y = concat_h O_h · W^O[head rows], then the all-reduce over the head-split devices
   const bool accumulate = (flags & TPLA_DECODE_ACCUMULATE) != 0;
-  e = run_wo_tc(static_cast<const uint16_t*>(w->W_O), Ob, g.D, p.Kf, L, part, y, accumulate,
-                comm ? nullptr : static_cast<uint16_t*>(out), s);
-  if (e != cudaSuccess) return cuda_fail(e, "K8 W^O");
+  e = launch_gemm_tn(static_cast<const uint16_t*>(w->W_O), Ob, p.Kf, g.D, p.Kf, L, y, accumulate,
+                     comm ? nullptr : static_cast<uint16_t*>(out), s);
+  if (e != cudaSuccess) return cuda_fail(e, "K9 W^O");
   if (comm) {
     ncclResult_t r = g_nccl.AllReduce(y, y, size_t(L) * g.D, ncclFloat32, ncclSum, comm->comm, s);
     if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));

@@ -79,13 +79,24 @@ def run_fwd(L, k, iters, dev):
 
     ms = timed(step, iters)
     ms_fwd = timed(fwd_only, iters)
+    abi.tpla_profile_reset()
+    abi.tpla_profile_enable(1)                               # per-kernel device time of one forward (all ranks)
+    fwd_only()
+    torch.cuda.synchronize()
+    prof = abi.profile_table()
+    abi.tpla_profile_enable(0)
+    abi.tpla_profile_reset()
+    kernels = {n: round(v[0] * 1e3 / k, 1) for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
     H = dims.h_q // k
     flops = (2 * 2 * L * dims.d_c * H * dims.d_h                       # k, v up-projections
              + 2 * (L * (L + 1) // 2) * H * (dims.d_h + dims.d_r + dims.d_h)   # causal QK (192) + PV (128)
              + 2 * L * H * dims.d_h * dims.D)                          # W^O
     return {"L": L, "k": k, "us_all_ranks": ms * 1e3, "us_per_device": ms * 1e3 / k,
             "fwd_us_per_device": ms_fwd * 1e3 / k, "fwd_tflops": flops / (ms_fwd / k / 1e3) / 1e12,
-            "fwd_gflop_per_device": flops / 1e9, "prompt_tokens_per_s_per_device": L / (ms / k / 1e3)}
+            "fwd_gflop_per_device": flops / 1e9, "prompt_tokens_per_s_per_device": L / (ms / k / 1e3),
+            "fwd_kernels_us_per_device": kernels,
+            "attn_tflops": 2 * (L * (L + 1) // 2) * H * (dims.d_h + dims.d_r + dims.d_h) /
+                           (kernels.get("K8_prefill_fa", float("nan")) * 1e-6) / 1e12}
 
 
 def run(L, k, g, iters, dev):
