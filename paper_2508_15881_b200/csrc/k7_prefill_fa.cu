@@ -9,7 +9,8 @@
 // with the head dimension 128 (+ 64 RoPE) instead of the absorbed 512 (+ 64): ~3.4x fewer FLOPs
 // than attending to the latent directly (f1).
 //
-// One CTA per (128-query tile, head); queries are the MMA M dimension.  Per 128-key tile:
+// Persistent CTAs over (128-query tile, head) work items, longest first; queries are the MMA M
+// dimension.  Per 128-key tile:
 //   QK  S[128 x 128] fp32 (TMEM) = Q [128 x 192] (smem) x [K ‖ k^PE] tileᵀ (smem, K-major)   tcgen05 SS
 //   softmax: 4 warps (one per TMEM lane quadrant, thread = query row), exact row max, lazily raised
 //            running max (O rescaled in TMEM only when it grows by > 2^8), P bf16 over S's columns
@@ -22,6 +23,8 @@
 // Warp roles (256 threads): w0 TMA, w1 MMA issuer, w2 TMEM allocator, w4-w7 softmax + epilogue.
 #include <cuda.h>
 #include <math.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "internal.h"
@@ -50,6 +53,16 @@ struct FaArgs {
   float scale_log2;
 };
 
+// work item i (longest first: the last query tiles attend to the most key tiles) -> (query tile, head)
+__device__ __forceinline__ void item_of(const FaArgs& a, int i, int& qt, int& h) {
+  qt = a.n_qt - 1 - i / a.H;
+  h = i % a.H;
+}
+
+// Persistent: CTA c takes work items c, c + G, c + 2G, ... (G = gridDim.x); the ring, S buffers and
+// their barrier phases run on over a CTA-global key-tile counter J, so one item's epilogue overlaps the
+// next item's first QKs: the next Q is loaded once the last QK of the item completed (q_free), and the
+// first PV of the next item (which overwrites O) waits for the epilogue's O loads (o_free).
 __global__ void __launch_bounds__(kThreads, 1)
 attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mqp,
                        const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mkp,
@@ -59,18 +72,17 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* s_q = smem;
   uint8_t* s_kv = smem + kQBytes;
-  __shared__ uint64_t q_full, kv_full[kStages], kv_empty[kStages], s_full[2], p_full[2], pv_done[2];
+  __shared__ uint64_t q_full, q_free, o_free, kv_full[kStages], kv_empty[kStages], s_full[2], p_full[2], pv_done[2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // longest first: the last query tiles attend to the most key tiles
-  const int qt = a.n_qt - 1 - int(blockIdx.x) / a.H, h = int(blockIdx.x) % a.H;
-  const int q0 = qt * kT;
-  const int n_kt = qt + 1;                      // key tiles 0..qt (causal)
+  const int n_items = a.n_qt * a.H, G = int(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mq); tma_prefetch_desc(&mqp); tma_prefetch_desc(&mk); tma_prefetch_desc(&mkp);
     tma_prefetch_desc(&mv);
     mbar_init(&q_full, 1);
+    mbar_init(&q_free, 1);
+    mbar_init(&o_free, 4);
     for (int i = 0; i < kStages; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&pv_done[i], 1); }
     fence_barrier_init();
@@ -85,161 +97,190 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (elect_one()) {
-      mbar_arrive_expect_tx(&q_full, kQBytes);
-      const int qc = (a.q_head0 + h) * 128, qpc = (a.q_head0 + h) * 64;
-      tma_load_2d(s_q, &mq, qc, q0, &q_full, kEvictFirst);
-      tma_load_2d(s_q + kBox, &mq, qc + 64, q0, &q_full, kEvictFirst);
-      tma_load_2d(s_q + 2 * kBox, &mqp, qpc, q0, &q_full, kEvictFirst);
-      for (int j = 0; j < n_kt; ++j) {
-        const int st = j % kStages;
-        mbar_wait(&kv_empty[st], ((j / kStages) & 1) ^ 1);
-        uint8_t* dst = s_kv + st * kStageBytes;
-        mbar_arrive_expect_tx(&kv_full[st], kStageBytes);
-        const int t0 = j * kT, kc = h * 128;
-        tma_load_2d(dst, &mk, kc, t0, &kv_full[st], kEvictNormal);              // K: re-read by every query tile
-        tma_load_2d(dst + kBox, &mk, kc + 64, t0, &kv_full[st], kEvictNormal);
-        tma_load_2d(dst + 2 * kBox, &mkp, 0, t0, &kv_full[st], kEvictNormal);     // k^PE (shared by the heads)
-        tma_load_2d(dst + 3 * kBox, &mv, kc, t0, &kv_full[st], kEvictNormal);
-        tma_load_2d(dst + 4 * kBox, &mv, kc + 64, t0, &kv_full[st], kEvictNormal);
+      int J = 0;
+      for (int it = 0, i = blockIdx.x; i < n_items; ++it, i += G) {
+        int qt, h;
+        item_of(a, i, qt, h);
+        if (it > 0) mbar_wait(&q_free, (it - 1) & 1);   // the previous item's QKs are complete
+        mbar_arrive_expect_tx(&q_full, kQBytes);
+        const int qc = (a.q_head0 + h) * 128, qpc = (a.q_head0 + h) * 64;
+        tma_load_2d(s_q, &mq, qc, qt * kT, &q_full, kEvictFirst);
+        tma_load_2d(s_q + kBox, &mq, qc + 64, qt * kT, &q_full, kEvictFirst);
+        tma_load_2d(s_q + 2 * kBox, &mqp, qpc, qt * kT, &q_full, kEvictFirst);
+        for (int j = 0; j <= qt; ++j, ++J) {           // key tiles 0..qt (causal)
+          const int st = J % kStages;
+          mbar_wait(&kv_empty[st], ((J / kStages) & 1) ^ 1);
+          uint8_t* dst = s_kv + st * kStageBytes;
+          mbar_arrive_expect_tx(&kv_full[st], kStageBytes);
+          const int t0 = j * kT, kc = h * 128;
+          tma_load_2d(dst, &mk, kc, t0, &kv_full[st], kEvictNormal);              // K: re-read by every query tile
+          tma_load_2d(dst + kBox, &mk, kc + 64, t0, &kv_full[st], kEvictNormal);
+          tma_load_2d(dst + 2 * kBox, &mkp, 0, t0, &kv_full[st], kEvictNormal);     // k^PE (shared by the heads)
+          tma_load_2d(dst + 3 * kBox, &mv, kc, t0, &kv_full[st], kEvictNormal);
+          tma_load_2d(dst + 4 * kBox, &mv, kc + 64, t0, &kv_full[st], kEvictNormal);
+        }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ---------------------------------------------------------------- MMA issuer: QK(j), then PV(j - 1)
+    // ---------------------------------------------------------------- MMA issuer: QK(J), then PV(J - 1)
     constexpr uint32_t id_qk = idesc_bf16(128, kT, false, false);
     constexpr uint32_t id_pv = idesc_bf16(128, 128, false, true);
     constexpr uint32_t hi_k = desc_sw128_hi(1024);
     const uint32_t q_addr = smem_addr(s_q), kv0 = smem_addr(s_kv);
-    auto issue_pv = [&](int j) {
-      mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+    auto issue_pv = [&](int J, bool first) {
+      mbar_wait(&p_full[J & 1], (J >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const int st = j % kStages;
+        const int st = J % kStages;
         // V: two 64-column MN-major atoms one box apart; 16 keys (2 KB) per k-step
         const uint64_t v_desc = make_desc(kv0 + st * kStageBytes + 3 * kBox, kBox, hi_k);
-        const uint32_t p_tmem = tb + kS0 + (j & 1) * kT;
+        const uint32_t p_tmem = tb + kS0 + (J & 1) * kT;
 #pragma unroll
         for (int kk = 0; kk < kT / 16; ++kk)
-          mma_ts(tb + kO, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), id_pv, (j == 0 && kk == 0) ? 0u : 1u);
+          mma_ts(tb + kO, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), id_pv, (first && kk == 0) ? 0u : 1u);
         mma_commit(&kv_empty[st]);
-        mma_commit(&pv_done[j & 1]);
+        mma_commit(&pv_done[J & 1]);
       }
       __syncwarp();
     };
-    mbar_wait(&q_full, 0);
-    for (int j = 0; j < n_kt; ++j) {
-      const int st = j % kStages;
-      mbar_wait(&kv_full[st], (j / kStages) & 1);
-      if (j >= 2) mbar_wait(&pv_done[j & 1], ((j - 2) >> 1) & 1);   // S buffer (= P of tile j - 2) free
-      tc_fence_after();
-      if (elect_one()) {
-        const uint64_t kd = make_desc(kv0 + st * kStageBytes, 16, hi_k);
-        const uint64_t qd = make_desc(q_addr, 16, hi_k);
-        const uint32_t s_tmem = tb + kS0 + (j & 1) * kT;
+    int J = 0;
+    for (int it = 0, i = blockIdx.x; i < n_items; ++it, i += G) {
+      int qt, h;
+      item_of(a, i, qt, h);
+      mbar_wait(&q_full, it & 1);
+      const int J0 = J;
+      for (int j = 0; j <= qt; ++j, ++J) {
+        const int st = J % kStages;
+        mbar_wait(&kv_full[st], (J / kStages) & 1);
+        if (J >= 2) mbar_wait(&pv_done[J & 1], ((J - 2) >> 1) & 1);   // S buffer (= P of tile J - 2) free
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t kd = make_desc(kv0 + st * kStageBytes, 16, hi_k);
+          const uint64_t qd = make_desc(q_addr, 16, hi_k);
+          const uint32_t s_tmem = tb + kS0 + (J & 1) * kT;
 #pragma unroll
-        for (int kk = 0; kk < 12; ++kk) {        // 192 = q (128) ‖ q^PE (64): box kk/4, +32 B per k-step
-          const uint64_t off = uint64_t(((kk >> 2) * kBox + (kk & 3) * 32) >> 4);
-          mma_ss(s_tmem, qd + off, kd + off, id_qk, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < 12; ++kk) {        // 192 = q (128) ‖ q^PE (64): box kk/4, +32 B per k-step
+            const uint64_t off = uint64_t(((kk >> 2) * kBox + (kk & 3) * 32) >> 4);
+            mma_ss(s_tmem, qd + off, kd + off, id_qk, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&s_full[J & 1]);
+          if (j == qt) mma_commit(&q_free);        // Q may be replaced once this QK completed
         }
-        mma_commit(&s_full[j & 1]);
+        __syncwarp();
+        if (j >= 1) issue_pv(J - 1, J - 1 == J0);
+        else if (it > 0) mbar_wait(&o_free, (it - 1) & 1);   // the previous item's O has been read
       }
-      __syncwarp();
-      if (j >= 1) issue_pv(j - 1);
+      issue_pv(J - 1, J - 1 == J0);
     }
-    issue_pv(n_kt - 1);
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- softmax + epilogue
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;                  // query row of the tile = TMEM lane
-    const int qi = q0 + r;                         // its token index
     const uint32_t lane_base = tb + (uint32_t(q4 * 32) << 16);
     const float sc = a.scale_log2;
-    float m_run = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kt; ++j) {
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t sv[4][32];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) tmem_ld32(lane_base + kS0 + (j & 1) * kT + 32 * q, sv[q]);
-      tmem_ld_wait();
-      float* x = reinterpret_cast<float*>(&sv[0][0]);
-      if (j == n_kt - 1) {                         // the diagonal tile: key t <= query i (t, i < L)
-        const int lim = min(qi, a.L - 1) - j * kT;
-#pragma unroll
-        for (int c = 0; c < kT; ++c) x[c] = c <= lim ? x[c] : -INFINITY;
-      }
-      float m0 = x[0], m1 = x[1], m2 = x[2], m3 = x[3];
-#pragma unroll
-      for (int c = 4; c < kT; c += 4) {
-        m0 = fmaxf(m0, x[c]); m1 = fmaxf(m1, x[c + 1]); m2 = fmaxf(m2, x[c + 2]); m3 = fmaxf(m3, x[c + 3]);
-      }
-      const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sc;
-      const float m_new = mx > m_run + kRescale ? mx : m_run;
-      const bool grow = j > 0 && m_new != m_run;
-      if (__any_sync(0xffffffffu, grow)) {         // O holds PV(j - 1) and earlier at m_run
-        const float f = grow ? ex2(m_run - m_new) : 1.f;
-        mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+    int J = 0;
+    for (int it = 0, i = blockIdx.x; i < n_items; ++it, i += G) {
+      int qt, h;
+      item_of(a, i, qt, h);
+      const int qi = qt * kT + r;                  // this row's token index
+      float m_run = -INFINITY, l = 0.f;
+      for (int j = 0; j <= qt; ++j, ++J) {
+        mbar_wait(&s_full[J & 1], (J >> 1) & 1);
         tc_fence_after();
-#pragma unroll 1
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          uint32_t ov[32];
-          tmem_ld32(lane_base + kO + c0, ov);
-          tmem_ld_wait();
+        uint32_t sv[4][32];
 #pragma unroll
-          for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * f);
-          tmem_st32(lane_base + kO + c0, ov);
+        for (int q = 0; q < 4; ++q) tmem_ld32(lane_base + kS0 + (J & 1) * kT + 32 * q, sv[q]);
+        tmem_ld_wait();
+        float* x = reinterpret_cast<float*>(&sv[0][0]);
+        if (j == qt) {                               // the diagonal tile: key t <= query i (t, i < L)
+          const int lim = min(qi, a.L - 1) - j * kT;
+#pragma unroll
+          for (int c = 0; c < kT; ++c) x[c] = c <= lim ? x[c] : -INFINITY;
         }
-        l *= f;
-      }
-      m_run = m_new;
-      const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
-      const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(neg_m, neg_m);
-      uint64_t l01 = f2_pack(0.f, 0.f), l23 = f2_pack(0.f, 0.f);
-      uint32_t pw[64];
+        float m0 = x[0], m1 = x[1], m2 = x[2], m3 = x[3];
 #pragma unroll
-      for (int c = 0; c < 64; c += 2) {
-        float y0, y1, y2, y3;
-        f2_unpack(ffma2(f2_pack(x[2 * c], x[2 * c + 1]), sc2, nm2), y0, y1);
-        f2_unpack(ffma2(f2_pack(x[2 * c + 2], x[2 * c + 3]), sc2, nm2), y2, y3);
-        const float p0 = ex2(y0), p1 = ex2(y1), p2 = ex2(y2), p3 = ex2(y3);
-        l01 = fadd2(l01, f2_pack(p0, p1));
-        l23 = fadd2(l23, f2_pack(p2, p3));
-        pw[c] = pack_bf16x2(p0, p1);
-        pw[c + 1] = pack_bf16x2(p2, p3);
+        for (int c = 4; c < kT; c += 4) {
+          m0 = fmaxf(m0, x[c]); m1 = fmaxf(m1, x[c + 1]); m2 = fmaxf(m2, x[c + 2]); m3 = fmaxf(m3, x[c + 3]);
+        }
+        const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sc;
+        const float m_new = mx > m_run + kRescale ? mx : m_run;
+        const bool grow = j > 0 && m_new != m_run;
+        if (__any_sync(0xffffffffu, grow)) {         // O holds PV(J - 1) and earlier at m_run
+          const float f = grow ? ex2(m_run - m_new) : 1.f;
+          mbar_wait(&pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c0 = 0; c0 < 128; c0 += 32) {
+            uint32_t ov[32];
+            tmem_ld32(lane_base + kO + c0, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * f);
+            tmem_st32(lane_base + kO + c0, ov);
+          }
+          l *= f;
+        }
+        m_run = m_new;
+        const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
+        const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(neg_m, neg_m);
+        uint64_t l01 = f2_pack(0.f, 0.f), l23 = f2_pack(0.f, 0.f);
+        uint32_t pw[64];
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+          float y0, y1, y2, y3;
+          f2_unpack(ffma2(f2_pack(x[2 * c], x[2 * c + 1]), sc2, nm2), y0, y1);
+          f2_unpack(ffma2(f2_pack(x[2 * c + 2], x[2 * c + 3]), sc2, nm2), y2, y3);
+          const float p0 = ex2(y0), p1 = ex2(y1);
+          float p2, p3;
+          if ((c & 6) == 0) {
+            ex2_poly2(y2, y3, p2, p3);               // 1 in 8 on the FMA pipe (arguments <= 8)
+          } else {
+            p2 = ex2(y2);
+            p3 = ex2(y3);
+          }
+          l01 = fadd2(l01, f2_pack(p0, p1));
+          l23 = fadd2(l23, f2_pack(p2, p3));
+          pw[c] = pack_bf16x2(p0, p1);
+          pw[c + 1] = pack_bf16x2(p2, p3);
+        }
+        float a0, a1, a2, a3;
+        f2_unpack(l01, a0, a1);
+        f2_unpack(l23, a2, a3);
+        l += (a0 + a1) + (a2 + a3);
+        // P (bf16 pairs) over S's first 64 columns
+        tmem_st32(lane_base + kS0 + (J & 1) * kT, *reinterpret_cast<uint32_t(*)[32]>(&pw[0]));
+        tmem_st32(lane_base + kS0 + (J & 1) * kT + 32, *reinterpret_cast<uint32_t(*)[32]>(&pw[32]));
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[J & 1]);
       }
-      float a0, a1, a2, a3;
-      f2_unpack(l01, a0, a1);
-      f2_unpack(l23, a2, a3);
-      l += (a0 + a1) + (a2 + a3);
-      // P (bf16 pairs) over S's first 64 columns
-      tmem_st32(lane_base + kS0 + (j & 1) * kT, *reinterpret_cast<uint32_t(*)[32]>(&pw[0]));
-      tmem_st32(lane_base + kS0 + (j & 1) * kT + 32, *reinterpret_cast<uint32_t(*)[32]>(&pw[32]));
-      tmem_st_wait();
+      // ---- epilogue: O / l -> bf16 [L, H * 128], then O is free for the next item's first PV
+      mbar_wait(&pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
+      tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      uint16_t* orow = a.o + (long)qi * a.H * 128 + h * 128;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t ov[32];
+        tmem_ld32(lane_base + kO + c0, ov);
+        tmem_ld_wait();
+        if (qi < a.L) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) {
+            uint4 u;
+            u.x = pack_bf16(__uint_as_float(ov[c]) * inv, __uint_as_float(ov[c + 1]) * inv);
+            u.y = pack_bf16(__uint_as_float(ov[c + 2]) * inv, __uint_as_float(ov[c + 3]) * inv);
+            u.z = pack_bf16(__uint_as_float(ov[c + 4]) * inv, __uint_as_float(ov[c + 5]) * inv);
+            u.w = pack_bf16(__uint_as_float(ov[c + 6]) * inv, __uint_as_float(ov[c + 7]) * inv);
+            *reinterpret_cast<uint4*>(orow + c0 + c) = u;
+          }
+        }
+      }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[j & 1]);
-    }
-    // ---- epilogue: O / l -> bf16 [L, H * 128]
-    mbar_wait(&pv_done[(n_kt - 1) & 1], ((n_kt - 1) >> 1) & 1);
-    tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    uint16_t* orow = a.o + (long)qi * a.H * 128 + h * 128;
-#pragma unroll 1
-    for (int c0 = 0; c0 < 128; c0 += 32) {
-      uint32_t ov[32];
-      tmem_ld32(lane_base + kO + c0, ov);
-      tmem_ld_wait();
-      if (qi < a.L) {
-#pragma unroll
-        for (int c = 0; c < 32; c += 8) {
-          uint4 u;
-          u.x = pack_bf16(__uint_as_float(ov[c]) * inv, __uint_as_float(ov[c + 1]) * inv);
-          u.y = pack_bf16(__uint_as_float(ov[c + 2]) * inv, __uint_as_float(ov[c + 3]) * inv);
-          u.z = pack_bf16(__uint_as_float(ov[c + 4]) * inv, __uint_as_float(ov[c + 5]) * inv);
-          u.w = pack_bf16(__uint_as_float(ov[c + 6]) * inv, __uint_as_float(ov[c + 7]) * inv);
-          *reinterpret_cast<uint4*>(orow + c0 + c) = u;
-        }
-      }
+      if (lane == 0) mbar_arrive(&o_free);
     }
   }
   tc_fence_before();
@@ -328,8 +369,12 @@ cudaError_t launch_attn_fwd_causal(const uint16_t* q_nope, const uint16_t* q_pe,
   a.n_qt = (L + kT - 1) / kT;
   a.q_head0 = q_head0;
   a.scale_log2 = sm_scale * 1.4426950408889634f;
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::max(1, std::min(a.n_qt * H, sms > 0 ? sms : 148));
   KernelScope ks("K8_prefill_fa", s);
-  return launch_k(attn_fwd_causal_kernel, a.n_qt * H, kThreads, kSmem, s, mq, mqp, mk, mkp, mv, a);
+  return launch_k(attn_fwd_causal_kernel, grid, kThreads, kSmem, s, mq, mqp, mk, mkp, mv, a);
 }
 
 }  // namespace tpla
