@@ -12,7 +12,8 @@
 // Persistent CTAs over (128-query tile, head) work items, longest first; queries are the MMA M
 // dimension.  Per 128-key tile:
 //   QK  S[128 x 128] fp32 (TMEM) = Q [128 x 192] (smem) x [K ‖ k^PE] tileᵀ (smem, K-major)   tcgen05 SS
-//   softmax: 4 warps (one per TMEM lane quadrant, thread = query row), exact row max, lazily raised
+//   softmax: 8 warps (two per TMEM lane quadrant, 64 columns each, thread = query row), exact row max
+//            (half maxima exchanged through smem), lazily raised
 //            running max (O rescaled in TMEM only when it grows by > 2^8), P bf16 over S's columns
 //   PV  O[128 x 128] (TMEM) += P (TMEM) x V tile (smem, MN-major)                          tcgen05 TS
 // Q, K, k^PE and V tiles arrive by TMA (SWIZZLE_128B, 128-row x 64-column boxes); two K/V stages and
@@ -20,7 +21,8 @@
 // diagonal tile is masked per row; tiles past it are never loaded (causal).  CTAs are issued
 // longest-first (the last query tiles attend to the most keys).
 //
-// Warp roles (256 threads): w0 TMA, w1 MMA issuer, w2 TMEM allocator, w4-w7 softmax + epilogue.
+// Warp roles (384 threads): w0 TMA (Q, K ring), w1 MMA issuer, w2 TMEM allocator, w3 TMA (V ring),
+// w4-w11 softmax + epilogue.
 #include <cuda.h>
 #include <math.h>
 
@@ -38,10 +40,11 @@ using namespace sm100;
 constexpr int kT = 128;               // queries per CTA = keys per tile
 constexpr int kBox = kT * 128;        // one [128 rows x 64 cols] bf16 box, 16 KB
 constexpr int kQBytes = 3 * kBox;     // q (2 boxes) + q^PE (1 box)
-constexpr int kStageBytes = 5 * kBox; // K (2 boxes), k^PE (1), V (2)
-constexpr int kStages = 2;
-constexpr int kSmem = 1024 + kQBytes + kStages * kStageBytes;
-constexpr int kThreads = 256;
+constexpr int kKBytes = 3 * kBox;     // K (2 boxes) + k^PE (1): a K-ring stage
+constexpr int kVBytes = 2 * kBox;     // V (2 boxes): a V-ring stage
+constexpr int kStages = 2;            // per ring
+constexpr int kSmem = 1024 + kQBytes + kStages * (kKBytes + kVBytes);
+constexpr int kThreads = 384;
 constexpr float kRescale = 8.0f;      // log2 units (p <= 2^8 between running-max raises)
 // TMEM columns: S0, S1 (128 each), O (128)
 constexpr int kS0 = 0, kO = 256, kTmemCols = 512;
@@ -53,10 +56,12 @@ struct FaArgs {
   float scale_log2;
 };
 
-// work item i (longest first: the last query tiles attend to the most key tiles) -> (query tile, head)
+// work item i -> (query tile, head): head-major, so the ~148 items in flight at any time cover only a
+// few heads and their K / V tiles (2 MB per head at 4K tokens) stay in L2 (query-tile-major order made
+// every CTA stream a different head's K / V from HBM); within a head the longest query tiles first
 __device__ __forceinline__ void item_of(const FaArgs& a, int i, int& qt, int& h) {
-  qt = a.n_qt - 1 - i / a.H;
-  h = i % a.H;
+  h = i / a.n_qt;
+  qt = a.n_qt - 1 - i % a.n_qt;
 }
 
 // Persistent: CTA c takes work items c, c + G, c + 2G, ... (G = gridDim.x); the ring, S buffers and
@@ -71,9 +76,13 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* s_q = smem;
-  uint8_t* s_kv = smem + kQBytes;
-  __shared__ uint64_t q_full, q_free, o_free, kv_full[kStages], kv_empty[kStages], s_full[2], p_full[2], pv_done[2];
+  uint8_t* s_k = smem + kQBytes;                 // K ring: [K ‖ k^PE] tiles, freed when their QK completes
+  uint8_t* s_v = s_k + kStages * kKBytes;        // V ring: freed when the tile's PV completes
+  __shared__ uint64_t q_full, q_free, o_free, k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
+  __shared__ uint64_t s_full[2], p_full[2], pv_done[2];
   __shared__ uint32_t tmem_base;
+  __shared__ float red_max[2][2][128];           // [J & 1][half][row] half-row maxima
+  __shared__ float red_l[2][128];                // [half][row] half-row sums at an item's end
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = a.n_qt * a.H, G = int(gridDim.x);
 
@@ -82,9 +91,11 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
     tma_prefetch_desc(&mv);
     mbar_init(&q_full, 1);
     mbar_init(&q_free, 1);
-    mbar_init(&o_free, 4);
-    for (int i = 0; i < kStages; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&pv_done[i], 1); }
+    mbar_init(&o_free, 8);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 8); mbar_init(&pv_done[i], 1); }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<kTmemCols>(&tmem_base);
@@ -94,30 +105,39 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
   tc_fence_after();
   const uint32_t tb = tmem_base;
 
-  if (warp == 0) {
-    // ---------------------------------------------------------------- TMA producer
+  if (warp == 0 || warp == 3) {
+    // ---------------------------------------------------------------- TMA producers: w0 Q + K ring, w3 V ring
+    // (two rings: the K tile of QK(J + 2) can land while PV(J) still holds V(J) — with one K/V stage
+    // released only by the PV, each QK waited for its tile's load latency, trace / ncu: tensor 32 %)
     if (elect_one()) {
       int J = 0;
       for (int it = 0, i = blockIdx.x; i < n_items; ++it, i += G) {
         int qt, h;
         item_of(a, i, qt, h);
-        if (it > 0) mbar_wait(&q_free, (it - 1) & 1);   // the previous item's QKs are complete
-        mbar_arrive_expect_tx(&q_full, kQBytes);
-        const int qc = (a.q_head0 + h) * 128, qpc = (a.q_head0 + h) * 64;
-        tma_load_2d(s_q, &mq, qc, qt * kT, &q_full, kEvictFirst);
-        tma_load_2d(s_q + kBox, &mq, qc + 64, qt * kT, &q_full, kEvictFirst);
-        tma_load_2d(s_q + 2 * kBox, &mqp, qpc, qt * kT, &q_full, kEvictFirst);
+        if (warp == 0) {
+          if (it > 0) mbar_wait(&q_free, (it - 1) & 1);   // the previous item's QKs are complete
+          mbar_arrive_expect_tx(&q_full, kQBytes);
+          const int qc = (a.q_head0 + h) * 128, qpc = (a.q_head0 + h) * 64;
+          tma_load_2d(s_q, &mq, qc, qt * kT, &q_full, kEvictFirst);
+          tma_load_2d(s_q + kBox, &mq, qc + 64, qt * kT, &q_full, kEvictFirst);
+          tma_load_2d(s_q + 2 * kBox, &mqp, qpc, qt * kT, &q_full, kEvictFirst);
+        }
         for (int j = 0; j <= qt; ++j, ++J) {           // key tiles 0..qt (causal)
-          const int st = J % kStages;
-          mbar_wait(&kv_empty[st], ((J / kStages) & 1) ^ 1);
-          uint8_t* dst = s_kv + st * kStageBytes;
-          mbar_arrive_expect_tx(&kv_full[st], kStageBytes);
-          const int t0 = j * kT, kc = h * 128;
-          tma_load_2d(dst, &mk, kc, t0, &kv_full[st], kEvictNormal);              // K: re-read by every query tile
-          tma_load_2d(dst + kBox, &mk, kc + 64, t0, &kv_full[st], kEvictNormal);
-          tma_load_2d(dst + 2 * kBox, &mkp, 0, t0, &kv_full[st], kEvictNormal);     // k^PE (shared by the heads)
-          tma_load_2d(dst + 3 * kBox, &mv, kc, t0, &kv_full[st], kEvictNormal);
-          tma_load_2d(dst + 4 * kBox, &mv, kc + 64, t0, &kv_full[st], kEvictNormal);
+          const int st = J % kStages, t0 = j * kT, kc = h * 128;
+          if (warp == 0) {
+            mbar_wait(&k_empty[st], ((J / kStages) & 1) ^ 1);
+            uint8_t* dst = s_k + st * kKBytes;
+            mbar_arrive_expect_tx(&k_full[st], kKBytes);
+            tma_load_2d(dst, &mk, kc, t0, &k_full[st], kEvictNormal);            // K: re-read by every query tile
+            tma_load_2d(dst + kBox, &mk, kc + 64, t0, &k_full[st], kEvictNormal);
+            tma_load_2d(dst + 2 * kBox, &mkp, 0, t0, &k_full[st], kEvictNormal);   // k^PE (shared by the heads)
+          } else {
+            mbar_wait(&v_empty[st], ((J / kStages) & 1) ^ 1);
+            uint8_t* dst = s_v + st * kVBytes;
+            mbar_arrive_expect_tx(&v_full[st], kVBytes);
+            tma_load_2d(dst, &mv, kc, t0, &v_full[st], kEvictNormal);
+            tma_load_2d(dst + kBox, &mv, kc + 64, t0, &v_full[st], kEvictNormal);
+          }
         }
       }
     }
@@ -127,19 +147,20 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
     constexpr uint32_t id_qk = idesc_bf16(128, kT, false, false);
     constexpr uint32_t id_pv = idesc_bf16(128, 128, false, true);
     constexpr uint32_t hi_k = desc_sw128_hi(1024);
-    const uint32_t q_addr = smem_addr(s_q), kv0 = smem_addr(s_kv);
+    const uint32_t q_addr = smem_addr(s_q), k0 = smem_addr(s_k), v0 = smem_addr(s_v);
     auto issue_pv = [&](int J, bool first) {
+      const int st = J % kStages;
       mbar_wait(&p_full[J & 1], (J >> 1) & 1);
+      mbar_wait(&v_full[st], (J / kStages) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const int st = J % kStages;
         // V: two 64-column MN-major atoms one box apart; 16 keys (2 KB) per k-step
-        const uint64_t v_desc = make_desc(kv0 + st * kStageBytes + 3 * kBox, kBox, hi_k);
+        const uint64_t v_desc = make_desc(v0 + st * kVBytes, kBox, hi_k);
         const uint32_t p_tmem = tb + kS0 + (J & 1) * kT;
 #pragma unroll
         for (int kk = 0; kk < kT / 16; ++kk)
           mma_ts(tb + kO, p_tmem + kk * 8, v_desc + uint64_t(kk * (2048 >> 4)), id_pv, (first && kk == 0) ? 0u : 1u);
-        mma_commit(&kv_empty[st]);
+        mma_commit(&v_empty[st]);
         mma_commit(&pv_done[J & 1]);
       }
       __syncwarp();
@@ -152,11 +173,11 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
       const int J0 = J;
       for (int j = 0; j <= qt; ++j, ++J) {
         const int st = J % kStages;
-        mbar_wait(&kv_full[st], (J / kStages) & 1);
+        mbar_wait(&k_full[st], (J / kStages) & 1);
         if (J >= 2) mbar_wait(&pv_done[J & 1], ((J - 2) >> 1) & 1);   // S buffer (= P of tile J - 2) free
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t kd = make_desc(kv0 + st * kStageBytes, 16, hi_k);
+          const uint64_t kd = make_desc(k0 + st * kKBytes, 16, hi_k);
           const uint64_t qd = make_desc(q_addr, 16, hi_k);
           const uint32_t s_tmem = tb + kS0 + (J & 1) * kT;
 #pragma unroll
@@ -165,6 +186,7 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
             mma_ss(s_tmem, qd + off, kd + off, id_qk, kk > 0 ? 1u : 0u);
           }
           mma_commit(&s_full[J & 1]);
+          mma_commit(&k_empty[st]);                // the K stage is free once this QK completed
           if (j == qt) mma_commit(&q_free);        // Q may be replaced once this QK completed
         }
         __syncwarp();
@@ -175,9 +197,14 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
     }
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- softmax + epilogue
-    const int q4 = warp & 3;
+    // Two warps per TMEM lane quadrant (warps 4+q and 8+q share SMSP q): warp `half` owns S columns
+    // [64 half, 64 half + 64) of every tile and O columns [64 half, ..); they exchange their half-row
+    // maxima through shared memory (named barrier per quadrant) so both take the same rescale
+    // decisions.  One warp alone reached ~2.8 of the SMSP's 4 exp/clk (tools/exps_rate), two ~3.7.
+    const int q4 = warp & 3, half = (warp - 4) >> 2;
     const int r = q4 * 32 + lane;                  // query row of the tile = TMEM lane
     const uint32_t lane_base = tb + (uint32_t(q4 * 32) << 16);
+    const uint32_t pair_bar = 1 + q4;
     const float sc = a.scale_log2;
     int J = 0;
     for (int it = 0, i = blockIdx.x; i < n_items; ++it, i += G) {
@@ -188,30 +215,34 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
       for (int j = 0; j <= qt; ++j, ++J) {
         mbar_wait(&s_full[J & 1], (J >> 1) & 1);
         tc_fence_after();
-        uint32_t sv[4][32];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) tmem_ld32(lane_base + kS0 + (J & 1) * kT + 32 * q, sv[q]);
+        uint32_t sv[2][32];
+        const uint32_t s_addr = lane_base + kS0 + (J & 1) * kT;
+        tmem_ld32(s_addr + 64 * half, sv[0]);
+        tmem_ld32(s_addr + 64 * half + 32, sv[1]);
         tmem_ld_wait();
         float* x = reinterpret_cast<float*>(&sv[0][0]);
         if (j == qt) {                               // the diagonal tile: key t <= query i (t, i < L)
-          const int lim = min(qi, a.L - 1) - j * kT;
+          const int lim = min(qi, a.L - 1) - j * kT - 64 * half;
 #pragma unroll
-          for (int c = 0; c < kT; ++c) x[c] = c <= lim ? x[c] : -INFINITY;
+          for (int c = 0; c < 64; ++c) x[c] = c <= lim ? x[c] : -INFINITY;
         }
         float m0 = x[0], m1 = x[1], m2 = x[2], m3 = x[3];
 #pragma unroll
-        for (int c = 4; c < kT; c += 4) {
+        for (int c = 4; c < 64; c += 4) {
           m0 = fmaxf(m0, x[c]); m1 = fmaxf(m1, x[c + 1]); m2 = fmaxf(m2, x[c + 2]); m3 = fmaxf(m3, x[c + 3]);
         }
-        const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sc;
+        float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+        red_max[J & 1][half][r] = mx;
+        named_bar_sync(pair_bar, 64);
+        mx = fmaxf(mx, red_max[J & 1][half ^ 1][r]) * sc;
         const float m_new = mx > m_run + kRescale ? mx : m_run;
         const bool grow = j > 0 && m_new != m_run;
-        if (__any_sync(0xffffffffu, grow)) {         // O holds PV(J - 1) and earlier at m_run
+        if (__any_sync(0xffffffffu, grow)) {         // O holds PV(J - 1) and earlier at m_run: this half
           const float f = grow ? ex2(m_run - m_new) : 1.f;
           mbar_wait(&pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll 1
-          for (int c0 = 0; c0 < 128; c0 += 32) {
+          for (int c0 = 64 * half; c0 < 64 * half + 64; c0 += 32) {
             uint32_t ov[32];
             tmem_ld32(lane_base + kO + c0, ov);
             tmem_ld_wait();
@@ -225,9 +256,9 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
         const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
         const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(neg_m, neg_m);
         uint64_t l01 = f2_pack(0.f, 0.f), l23 = f2_pack(0.f, 0.f);
-        uint32_t pw[64];
+        uint32_t pw[32];
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
+        for (int c = 0; c < 32; c += 2) {
           float y0, y1, y2, y3;
           f2_unpack(ffma2(f2_pack(x[2 * c], x[2 * c + 1]), sc2, nm2), y0, y1);
           f2_unpack(ffma2(f2_pack(x[2 * c + 2], x[2 * c + 3]), sc2, nm2), y2, y3);
@@ -248,21 +279,23 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
         f2_unpack(l01, a0, a1);
         f2_unpack(l23, a2, a3);
         l += (a0 + a1) + (a2 + a3);
-        // P (bf16 pairs) over S's first 64 columns
-        tmem_st32(lane_base + kS0 + (J & 1) * kT, *reinterpret_cast<uint32_t(*)[32]>(&pw[0]));
-        tmem_st32(lane_base + kS0 + (J & 1) * kT + 32, *reinterpret_cast<uint32_t(*)[32]>(&pw[32]));
+        // P (bf16 pairs) of this half: packed columns [32 half, 32 half + 32) of S (logits consumed)
+        tmem_st32(s_addr + 32 * half, pw);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[J & 1]);
       }
-      // ---- epilogue: O / l -> bf16 [L, H * 128], then O is free for the next item's first PV
+      // ---- epilogue: O / l -> bf16 [L, H * 128] (this half's 64 columns), then O is free
+      red_l[half][r] = l;
       mbar_wait(&pv_done[(J - 1) & 1], ((J - 1) >> 1) & 1);
       tc_fence_after();
-      const float inv = l > 0.f ? 1.f / l : 0.f;
+      named_bar_sync(pair_bar, 64);
+      const float lt = l + red_l[half ^ 1][r];
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
       uint16_t* orow = a.o + (long)qi * a.H * 128 + h * 128;
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
+      for (int c0 = 64 * half; c0 < 64 * half + 64; c0 += 32) {
         uint32_t ov[32];
         tmem_ld32(lane_base + kO + c0, ov);
         tmem_ld_wait();
@@ -278,6 +311,7 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
           }
         }
       }
+      named_bar_sync(pair_bar, 64);                 // red_l free again
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free);
