@@ -42,7 +42,8 @@ struct G9Args {
 };
 
 __global__ void __launch_bounds__(384, 1)
-gemm_tn_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mx, G9Args a) {
+gemm_tn_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mx,
+               const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap mo, G9Args a) {
   pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -105,29 +106,43 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ C
     const uint32_t lane_base = tb + m * kN + (uint32_t(q4 * 32) << 16);
     mbar_wait(&acc_full, 0);
     tc_fence_after();
-    const bool n_ok = n < a.N;
+    // Through shared memory and TMA: per 32-token chunk the warp stages its [32 tokens x 32 features]
+    // block (fp32 and / or bf16; the ring is free once acc_full fired) and one lane stores it with
+    // cp.async.bulk.tensor (or reduce-adds it into y); out-of-range rows / columns are clipped by the
+    // tensor maps.  (Per-thread 4-byte stores, three memory instructions per element with the
+    // accumulate, made the epilogue as long as a K = 512 main loop.)
+    const int wi = warp - 4;                     // 0..7
+    float* stg = reinterpret_cast<float*>(smem) + wi * 2 * 1024;               // 2 x [32 x 32] fp32
+    uint16_t* stg16 = reinterpret_cast<uint16_t*>(smem + 8 * 2 * 4096) + wi * 2 * 1024;   // 2 x [32 x 32] bf16
+    const int n0 = (rp * kMT + m) * kM + q4 * 32;
 #pragma unroll 1
-    for (int c0 = 0; c0 < kN; c0 += 32) {
+    for (int c = 0; c < kN / 32; ++c) {
       uint32_t d[32];
-      tmem_ld32(lane_base + c0, d);
+      tmem_ld32(lane_base + 32 * c, d);
       tmem_ld_wait();
-      const int t0 = tt * kN + c0;
-      if (n_ok) {
+      if (lane == 0) bulk_wait_read<1>();        // this chunk's staging buffer (used two chunks ago) is read
+      __syncwarp();
+      float* bf = stg + (c & 1) * 1024;
+      uint16_t* bh = stg16 + (c & 1) * 1024;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int t = t0 + j;
-          if (t < a.L) {
-            float v = __uint_as_float(d[j]);
-            const long i = (long)t * a.N + n;
-            if (a.y) {
-              if (a.accumulate) v += a.y[i];
-              a.y[i] = v;
-            }
-            if (a.out) a.out[i] = f2bf(v);
-          }
+      for (int j = 0; j < 32; ++j) {             // row j = token, column lane = feature: conflict-free
+        if (a.y) bf[j * 32 + lane] = __uint_as_float(d[j]);
+        if (a.out && !(a.y && a.accumulate)) bh[j * 32 + lane] = f2bf(__uint_as_float(d[j]));
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int t0 = tt * kN + 32 * c;
+        if (a.y) {
+          if (a.accumulate) tma_reduce_add_2d(&my, n0, t0, bf);
+          else tma_store_2d(&my, n0, t0, bf);
         }
+        if (a.out && !(a.y && a.accumulate)) tma_store_2d(&mo, n0, t0, bh);
+        bulk_commit();
       }
     }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -139,7 +154,9 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-bool map2d(CUtensorMap* m, const void* base, long cols, long rows, long ld, int box_r) {
+bool map2d(CUtensorMap* m, const void* base, long cols, long rows, long ld, int box_r, int box_c = kK,
+           CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, int esize = 2,
+           CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   static EncodeFn fn = nullptr;
   if (!fn) {
     void* p = nullptr;
@@ -150,12 +167,11 @@ bool map2d(CUtensorMap* m, const void* base, long cols, long rows, long ld, int 
   }
   if (!fn) return false;
   cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
-  cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
-  cuuint32_t box[2] = {cuuint32_t(kK), cuuint32_t(box_r)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * esize};
+  cuuint32_t box[2] = {cuuint32_t(box_c), cuuint32_t(box_r)};
   cuuint32_t es[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -165,8 +181,13 @@ bool gemm_tn_supported(int N, int K) { return N >= 1 && K >= kK && K % kK == 0; 
 cudaError_t launch_gemm_tn(const uint16_t* Wt, const uint16_t* X, long ld_x, int N, int K, int L, float* y,
                            bool accumulate, uint16_t* out, cudaStream_t s) {
   const int n_rt = (N + kM - 1) / kM, n_tt = (L + kN - 1) / kN, n_rp = (n_rt + kMT - 1) / kMT;
-  CUtensorMap mw, mx;
+  if (y && accumulate && out) return cudaErrorInvalidValue;   // (the bf16 copy of an accumulated y: not here)
+  CUtensorMap mw, mx, my{}, mo{};
   if (!map2d(&mw, Wt, kK, long(n_rt) * (K / kK) * kM, kK, kM) || !map2d(&mx, X, K, L, ld_x, kN))
+    return cudaErrorInvalidValue;
+  if (y && !map2d(&my, y, N, L, N, 32, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  if (out && !map2d(&mo, out, N, L, N, 32, 32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
@@ -176,7 +197,7 @@ cudaError_t launch_gemm_tn(const uint16_t* Wt, const uint16_t* X, long ld_x, int
   }
   G9Args a{y, out, N, L, K / kK, n_tt, n_rt, accumulate ? 1 : 0};
   KernelScope ks("K9_prefill_gemm", s);
-  return launch_k(gemm_tn_kernel, n_rp * n_tt, 384, kSmem, s, mw, mx, a);
+  return launch_k(gemm_tn_kernel, n_rp * n_tt, 384, kSmem, s, mw, mx, my, mo, a);
 }
 
 }  // namespace tpla

@@ -956,9 +956,14 @@ tpla_status tpla_prefill_mla_forward(const tpla_config* cfg, const tpla_prefill_
   if (e != cudaSuccess) return cuda_fail(e, "K8 attention");
   // y = concat_h O_h · W^O[head rows], then the all-reduce over the head-split devices
   const bool accumulate = (flags & TPLA_DECODE_ACCUMULATE) != 0;
+  uint16_t* out16 = comm ? nullptr : static_cast<uint16_t*>(out);
   e = launch_gemm_tn(static_cast<const uint16_t*>(w->W_O), Ob, p.Kf, g.D, p.Kf, L, y, accumulate,
-                     comm ? nullptr : static_cast<uint16_t*>(out), s);
+                     accumulate ? nullptr : out16, s);
   if (e != cudaSuccess) return cuda_fail(e, "K9 W^O");
+  if (accumulate && out16) {                     // (y was reduce-added: its bf16 copy after the sum)
+    e = launch_cast_bf16(y, long(L) * g.D, out16, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cast");
+  }
   if (comm) {
     ncclResult_t r = g_nccl.AllReduce(y, y, size_t(L) * g.D, ncclFloat32, ncclSum, comm->comm, s);
     if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
