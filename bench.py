@@ -84,6 +84,8 @@ def parse():
                    help="up-projection: 'rank' = every rank multiplies its own v_j by its W^O rows (P:139-141); "
                         "'shared' = the g ranks of a head block sum v first and read W^O once, reduce-scattered "
                         "across processes (SURVEY f2(ii)); auto = shared when g > 1")
+    p.add_argument("--no-fused-ar", action="store_true",
+                   help="N > 1: plain ncclAllReduce after the W^O GEMM instead of the fused one-shot all-reduce")
     p.add_argument("--no-rank-streams", action="store_true",
                    help="issue the co-located ranks of a latent group serially on one stream (default: one stream "
                         "per rank, separate v accumulators summed in tpla_project_out_sum)")
@@ -419,10 +421,17 @@ def main():
     y = torch.zeros((B * nq, dims.D), dtype=torch.float32, device=dev)
     out = torch.empty((B * nq, dims.D), dtype=torch.bfloat16, device=dev)
     comm = None
+    ar_mode = 0
     if N > 1:
         obj = [abi.tpla_comm_unique_id() if proc == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         comm = abi.tpla_comm_init(obj[0], N, proc)
+        if not args.no_fused_ar:
+            try:        # the all-reduce inside the K5 reduce (symmetric window, LSA / NVLS)
+                abi.tpla_comm_enable_fused_allreduce(comm, B * nq * dims.D)
+            except abi.TplaError as e:
+                print(f"[bench] fused all-reduce unavailable, plain ncclAllReduce: {e}", file=sys.stderr)
+        ar_mode = abi.tpla_comm_fused_allreduce_mode(comm)
     wo = args.wo if args.wo != "auto" else ("shared" if g > 1 else "rank")
     groups = head_block_groups(k, g, N, proc) if wo == "shared" else []
     gcomms = {}
@@ -757,6 +766,9 @@ def main():
                 "gpu_launches_per_step": launches / args.steps, "clocks": clk, "clocks_sustained": clocks_sust,
                 "kernels": kernels,
                 "cuda_graph": graph is not None, "rank_streams": any(par),
+                "all_reduce": ({0: "ncclAllReduce", 1: "fused into the K5 reduce (LSA peer loads)",
+                                2: "fused into the K5 reduce (NVLS multimem.ld_reduce)"}[ar_mode]
+                               if N > 1 else "none (N = 1)"),
                 "kernel_timing": ("library CUDA events (on the launching stream) captured as graph event nodes "
                                   "around every kernel of the K timed steps, replayed right after the timed "
                                   "replay, with the co-located ranks on ONE stream (the timed graph overlaps them "

@@ -319,6 +319,18 @@ tpla_status tpla_comm_unique_id(void* out128);
 /* Join the k-device communicator (blocking until all ranks join).  The current CUDA device
  * must already be this rank's GPU. */
 tpla_status tpla_comm_init(tpla_comm** out, const void* unique_id128, int32_t world, int32_t rank);
+/* Fused W^O epilogue + one-shot all-reduce (O = AllReduce(Σ_r Õ_r)):
+ * allocates a symmetric buffer of 2 · max_elems fp32 (ncclMemAlloc), registers it as an NCCL window
+ * (NCCL_WIN_COLL_SYMMETRIC) and creates a device communicator with LSA barriers (and the NVLS
+ * multicast address when the system has one).  COLLECTIVE: every rank of the communicator calls it.
+ * Afterwards the K5 segment reduce of tpla_decode / tpla_decode_mtp / tpla_project_out calls on this
+ * communicator whose R·D <= max_elems writes the rank's Õ rows into the buffer, meets the peers at an
+ * LSA barrier and sums the ranks itself (multimem.ld_reduce through the switch, else peer loads over
+ * NVLink in rank order) — no separate ncclAllReduce or cast launch.  TPLA_FUSED_AR=0 disables it per
+ * process, =unicast forbids the multicast.  TPLA_ERR_UNSUPPORTED if the loaded NCCL has no device API
+ * matching the headers (NCCL 2.28).  tpla_comm_fused_allreduce_mode: 0 off, 1 peer loads, 2 multicast. */
+tpla_status tpla_comm_enable_fused_allreduce(tpla_comm* comm, int64_t max_elems);
+int32_t tpla_comm_fused_allreduce_mode(const tpla_comm* comm);
 tpla_status tpla_comm_destroy(tpla_comm* comm);
 
 /* Synchronise `stream` and report any asynchronous CUDA fault. */

@@ -20,6 +20,16 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2508_15881_b200.build` "
                       "(no CPU fallback exists for the TPLA hot path)")
 
+if "TPLA_NCCL_LIB" not in os.environ:
+    # the device API (f2(i)) must match the NCCL headers the library was compiled with (2.28): prefer
+    # the NCCL that ships with torch over a system libnccl.so.2 found first on the loader path
+    try:
+        import nvidia.nccl  # type: ignore
+        _nccl = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        if os.path.exists(_nccl):
+            os.environ["TPLA_NCCL_LIB"] = _nccl
+    except Exception:
+        pass
 _lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
 
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_DIVISIBILITY, ERR_CAPACITY, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED = range(8)
@@ -104,6 +114,8 @@ _SIGS = {
     "tpla_prefill_mla_forward": ([C.POINTER(tpla_config), C.POINTER(tpla_prefill_weights), _P, _P, _P, _P, _I, _P, _S,
                                   _P, _P, _I, _P, _P], _I),
     "tpla_comm_unique_id": ([_P], _I),
+    "tpla_comm_enable_fused_allreduce": ([_P, C.c_int64], _I),
+    "tpla_comm_fused_allreduce_mode": ([_P], _I),
     "tpla_comm_init": ([C.POINTER(_P), _P, _I, _I], _I),
     "tpla_comm_destroy": ([_P], _I),
     "tpla_sync": ([_P], _I),
@@ -309,6 +321,17 @@ def tpla_comm_init(unique_id: bytes, world: int, rank: int):
     out = C.c_void_p()
     _check(_lib.tpla_comm_init(C.byref(out), C.cast(buf, C.c_void_p), world, rank), "tpla_comm_init")
     return out
+
+
+def tpla_comm_enable_fused_allreduce(comm, max_elems: int):
+    """symmetric window + device communicator for the fused W^O epilogue + one-shot
+    all-reduce (collective: every rank calls it)."""
+    _check(_lib.tpla_comm_enable_fused_allreduce(comm, max_elems), "tpla_comm_enable_fused_allreduce")
+
+
+def tpla_comm_fused_allreduce_mode(comm) -> int:
+    """0: plain ncclAllReduce, 1: fused with peer loads (LSA), 2: fused through the NVLS multicast."""
+    return int(_lib.tpla_comm_fused_allreduce_mode(comm))
 
 
 def tpla_comm_destroy(comm):

@@ -115,10 +115,25 @@ size_t wo_tc_part_bytes(int N, int K, int B);
 // out_bf16 (optional): also write bf16(y) (the step's output when no all-reduce follows)
 // [k_begin, k_begin + k_len): a 64-multiple slice of W^O's K rows (k_len 0 = all); v is then [B, k_len],
 // the slice's columns only (a rank projecting its share of a v summed over the latent group)
-// v_ld: v's row stride in elements (0: k_len, dense rows)
+// v_ld: v's row stride in elements (0: k_len, dense rows).  ar (optional): fuse the all-reduce into the
+// segment reduce (FusedAr below); ar_row0: the first row of this launch in the symmetric buffer.
+struct FusedAr;
 cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, void* part_ws, float* y,
                          bool accumulate, uint16_t* out_bf16, cudaStream_t s, int k_begin = 0, int k_len = 0,
-                         long v_ld = 0);
+                         long v_ld = 0, const FusedAr* ar = nullptr, long ar_row0 = 0);
+
+// Fused W^O epilogue + one-shot all-reduce: the segment reduce of K5 writes this rank's
+// Õ rows into a symmetric buffer (an NCCL window), every reduce CTA meets the same CTA of every peer at
+// an LSA barrier, then sums the k ranks' rows — through the NVLS multicast address (multimem.ld_reduce)
+// when the communicator has one, else by peer loads in rank order — into y (fp32) and the bf16 output.
+// The buffer is double-buffered by the barrier epoch (a rank can be at most one call ahead of a peer).
+constexpr int kArCtas = 128;          // reduce CTAs = LSA barriers of the device communicator
+struct FusedAr {
+  void* dev_comm;                     // ncclDevComm (host copy, passed by value to the kernel)
+  void* window;                       // ncclWindow_t
+  size_t half_elems;                  // fp32 elements per buffer half
+  int multimem;                       // use the NVLS multicast address
+};
 
 // K8: causal prefill attention, non-absorbed MLA (k7_prefill_fa.cu).  q_nope [L, h_q*128] and q_pe
 // [L, h_q*64] hold all heads (this device's head 0 is q_head0); K, V, O [L, H*128] bf16; k_pe rows of

@@ -14,6 +14,8 @@
 //
 // Warp roles (256 threads): w0 TMA, w1 MMA, w2 TMEM allocator, w4-w7 epilogue (TMEM lanes).
 #include <cuda.h>
+#include <nccl.h>
+#include <nccl_device.h>
 
 #include <algorithm>
 
@@ -194,6 +196,54 @@ __global__ void reduce_seg_kernel(const float* __restrict__ part, const int32_t*
   if (out) out[i] = f2bf(acc);
 }
 
+// The same reduce fused with the one-shot all-reduce over the symmetric buffer (FusedAr, SURVEY f2(i);
+// O = AllReduce(Σ_r Õ_r)): (1) this rank's rows of the launch -> its half of the buffer (the half
+// chosen by the barrier epoch: a rank can be one call ahead of a peer, never two); (2) the CTA meets
+// the same CTA index of every peer (LSA barrier, release / acquire at system scope); (3) every element of
+// the CTA's slice summed over the ranks — multimem.ld_reduce through the NVLS multicast address, or
+// peer loads over NVLink in rank order — into y and the bf16 output.  Fixed geometry: kArCtas CTAs,
+// so a CTA's slice is the same set of elements on every rank.
+__global__ void __launch_bounds__(256) reduce_seg_ar_kernel(const float* __restrict__ part,
+                                                            const int32_t* __restrict__ meta, int N, int B,
+                                                            float* __restrict__ y, int accumulate,
+                                                            uint16_t* __restrict__ out, ncclDevComm dc,
+                                                            ncclWindow_t win, size_t half_elems, long row0,
+                                                            int multimem) {
+  pdl_trigger();
+  pdl_wait();
+  ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x, multimem != 0);
+  const uint32_t step = multimem ? uint32_t(dc.lsaSize) : 1u;          // epoch advance per barrier
+  const size_t base = ((bar.epoch / step) & 1u) * half_elems + size_t(row0) * N;
+  float* mine = static_cast<float*>(ncclGetLocalPointer(win, 0)) + base;
+  const long n = (long)B * N;
+  for (long i = blockIdx.x * 256L + threadIdx.x; i < n; i += 256L * gridDim.x) {
+    const int b = int(i / N), nn = int(i % N), rt = nn / kTM;
+    float acc = accumulate ? y[i] : 0.f;
+    for (int s = meta[2 * rt]; s <= meta[2 * rt + 1]; ++s) acc += part[((long)s * B + b) * kTM + (nn % kTM)];
+    mine[i] = acc;
+  }
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  if (multimem) {
+    const float* mc = static_cast<const float*>(ncclGetLsaMultimemPointer(win, 0, dc)) + base;
+    for (long i = blockIdx.x * 256L + threadIdx.x; i < n; i += 256L * gridDim.x) {
+      float t;
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(t) : "l"(mc + i) : "memory");
+      y[i] = t;
+      if (out) out[i] = f2bf(t);
+    }
+  } else {
+    for (long i = blockIdx.x * 256L + threadIdx.x; i < n; i += 256L * gridDim.x) {
+      float t = 0.f;
+      for (int p = 0; p < dc.lsaSize; ++p)                             // fixed rank order: deterministic
+        t += static_cast<const float*>(ncclGetLsaPointer(win, 0, p))[base + i];
+      y[i] = t;
+      if (out) out[i] = f2bf(t);
+    }
+  }
+  // (no second barrier: this half is written again two calls later, and this CTA index of every peer
+  // must have arrived at the next call's barrier — after these reads — before that)
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -264,7 +314,8 @@ size_t wo_tc_part_bytes(int N, int K, int B) {
 }
 
 cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, int B, void* part_ws, float* y,
-                         bool accumulate, uint16_t* out_bf16, cudaStream_t s, int k_begin, int k_len, long v_ld) {
+                         bool accumulate, uint16_t* out_bf16, cudaStream_t s, int k_begin, int k_len, long v_ld,
+                         const FusedAr* ar, long ar_row0) {
   if (k_len <= 0) k_len = K;
   const int n_tiles = (N + kTM - 1) / kTM;
   const int NP = B <= 32 ? 32 : B <= 64 ? 64 : B <= 128 ? 128 : 256;
@@ -287,6 +338,12 @@ cudaError_t launch_wo_tc(const uint16_t* Wt, const uint16_t* v, int N, int K, in
   }
   if (e != cudaSuccess) return e;
   const long n = long(B) * N;
+  if (ar) {
+    KernelScope ks("K5_reduce_allreduce", s);
+    return launch_k(reduce_seg_ar_kernel, kArCtas, 256, 0, s, a.part, a.meta, N, B, y, accumulate ? 1 : 0, out_bf16,
+                    *static_cast<const ncclDevComm*>(ar->dev_comm), static_cast<ncclWindow_t>(ar->window),
+                    ar->half_elems, ar_row0, ar->multimem);
+  }
   KernelScope ks("K5_reduce", s);
   return launch_k(reduce_seg_kernel, int((n + 255) / 256), 256, 0, s, a.part, a.meta, N, B, y, accumulate ? 1 : 0,
                   out_bf16);

@@ -17,6 +17,7 @@
 
 #include "internal.h"
 #include "nccl.h"
+#include "nccl_device.h"
 
 namespace tpla {
 std::atomic<int64_t> g_launches{0};
@@ -155,6 +156,15 @@ struct NcclApi {
                                 cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // device API (NCCL >= 2.28; optional: the fused all-reduce of SURVEY f2(i))
+  ncclResult_t (*GetVersion)(int*) = nullptr;
+  ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void*) = nullptr;
+  ncclResult_t (*WinRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+  ncclResult_t (*WinDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
+  ncclResult_t (*DevCommCreate)(ncclComm_t, ncclDevCommRequirements_t const*, ncclDevComm_t*) = nullptr;
+  ncclResult_t (*DevCommDestroy)(ncclComm_t, ncclDevComm_t const*) = nullptr;
+  bool device_api = false;
 };
 NcclApi g_nccl;
 
@@ -176,6 +186,18 @@ bool load_nccl() {
   g_nccl.ReduceScatter = (decltype(g_nccl.ReduceScatter))dlsym(h, "ncclReduceScatter");
   g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.GetVersion = (decltype(g_nccl.GetVersion))dlsym(h, "ncclGetVersion");
+  g_nccl.MemAlloc = (decltype(g_nccl.MemAlloc))dlsym(h, "ncclMemAlloc");
+  g_nccl.MemFree = (decltype(g_nccl.MemFree))dlsym(h, "ncclMemFree");
+  g_nccl.WinRegister = (decltype(g_nccl.WinRegister))dlsym(h, "ncclCommWindowRegister");
+  g_nccl.WinDeregister = (decltype(g_nccl.WinDeregister))dlsym(h, "ncclCommWindowDeregister");
+  g_nccl.DevCommCreate = (decltype(g_nccl.DevCommCreate))dlsym(h, "ncclDevCommCreate");
+  g_nccl.DevCommDestroy = (decltype(g_nccl.DevCommDestroy))dlsym(h, "ncclDevCommDestroy");
+  int ver = 0;
+  // the device communicator's layout is the one of the headers this library was compiled with
+  g_nccl.device_api = g_nccl.GetVersion && g_nccl.GetVersion(&ver) == ncclSuccess && ver >= 22800 &&
+                      ver / 100 == NCCL_VERSION_CODE / 100 && g_nccl.MemAlloc && g_nccl.MemFree &&
+                      g_nccl.WinRegister && g_nccl.WinDeregister && g_nccl.DevCommCreate && g_nccl.DevCommDestroy;
   g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.ReduceScatter &&
              g_nccl.CommDestroy && g_nccl.GetErrorString;
   return g_nccl.ok;
@@ -186,7 +208,23 @@ bool load_nccl() {
 struct tpla_comm {
   ncclComm_t comm;
   int world, rank;
+  // fused W^O epilogue + one-shot all-reduce (tpla_comm_enable_fused_allreduce)
+  void* sym = nullptr;                 // ncclMemAlloc'd symmetric buffer (2 halves)
+  ncclWindow_t win = nullptr;
+  ncclDevComm dev{};
+  bool dev_ok = false;
+  tpla::FusedAr ar{};
 };
+
+namespace {
+// the fused path for a call of R rows of D outputs (or null: the plain ncclAllReduce follows)
+const tpla::FusedAr* fused_ar(const tpla_comm* c, long R, int D) {
+  if (!c || !c->ar.window) return nullptr;
+  static const char* env = getenv("TPLA_FUSED_AR");
+  if (env && env[0] == '0') return nullptr;
+  return size_t(R) * D <= c->ar.half_elems ? &c->ar : nullptr;
+}
+}  // namespace
 
 namespace tpla {
 
@@ -210,12 +248,13 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // chunk's GEMM waits for the previous chunk's reduce before writing it: PDL wait at entry).
 constexpr int kWoRows = 256;
 static cudaError_t run_wo_tc(const uint16_t* Wo, const uint16_t* v, int D, int K, int R, void* part, float* y,
-                             bool accumulate, uint16_t* out16, cudaStream_t s, int k_begin = 0, int k_len = 0) {
+                             bool accumulate, uint16_t* out16, cudaStream_t s, int k_begin = 0, int k_len = 0,
+                             const FusedAr* ar = nullptr) {
   const int kl = k_len > 0 ? k_len : K;             // v's row length (the K-slice's columns)
   for (int r0 = 0; r0 < R; r0 += kWoRows) {
     const int n = std::min(kWoRows, R - r0);
     cudaError_t e = launch_wo_tc(Wo, v + size_t(r0) * kl, D, K, n, part, y + size_t(r0) * D, accumulate,
-                                 out16 ? out16 + size_t(r0) * D : nullptr, s, k_begin, k_len);
+                                 out16 ? out16 + size_t(r0) * D : nullptr, s, k_begin, k_len, 0, ar, r0);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -597,13 +636,17 @@ tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const
   const bool accumulate = (flags & TPLA_DECODE_ACCUMULATE) != 0;
   const int Kw = g.h_loc * g.d_h;
   const char* force = getenv("TPLA_WO");
-  bool out_done = false;
+  bool out_done = false, reduced = false;
   if (wo_tc_supported(g.D, Kw, std::min(R, kWoRows)) && !(force && strcmp(force, "mma") == 0)) {
-    // without an all-reduce the segment reduce also writes the bf16 output (no cast launch)
-    uint16_t* out16 = comm ? nullptr : static_cast<uint16_t*>(out);
-    e = run_wo_tc(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, R, base + L.wo_part, y, accumulate, out16, s);
+    // without an all-reduce the segment reduce also writes the bf16 output (no cast launch); with the
+    // fused one-shot all-reduce (f2(i)) it also sums the ranks
+    const FusedAr* ar = fused_ar(comm, R, g.D);
+    uint16_t* out16 = (comm && !ar) ? nullptr : static_cast<uint16_t*>(out);
+    e = run_wo_tc(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, R, base + L.wo_part, y, accumulate, out16, s, 0,
+                  0, ar);
     if (e != cudaSuccess) return cuda_fail(e, "K5b W_O (tcgen05)");
     out_done = out16 != nullptr;
+    reduced = ar != nullptr;
   } else {
     e = launch_skinny_gemm(static_cast<const uint16_t*>(w->W_O), v, g.D, Kw, R, L.kslices, y_part, s);
     if (e != cudaSuccess) return cuda_fail(e, "K5b W_O");
@@ -611,7 +654,7 @@ tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const
     if (e != cudaSuccess) return cuda_fail(e, "K5b reduce");
   }
   // C1: O = AllReduce(Σ_r Õ_r)
-  if (comm) {
+  if (comm && !reduced) {
     ncclResult_t r = g_nccl.AllReduce(y, y, size_t(R) * g.D, ncclFloat32, ncclSum, comm->comm, s);
     if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
   }
@@ -793,11 +836,12 @@ static tpla_status project_out_common(const tpla_config* cfg, const tpla_weights
   cudaError_t e = n_v == 1 ? launch_cast_bf16(v_mine[0], long(R) * kc, v16, s, "K5_v_cast")
                            : launch_sum_cast_bf16(v_mine, n_v, long(R) * kc, v16, s);
   if (e != cudaSuccess) return cuda_fail(e, "v cast");
-  uint16_t* out16 = comm ? nullptr : static_cast<uint16_t*>(out);
+  const FusedAr* ar = fused_ar(comm, R, g.D);                     // f2(i): the all-reduce in the K5 reduce
+  uint16_t* out16 = (comm && !ar) ? nullptr : static_cast<uint16_t*>(out);
   e = run_wo_tc(static_cast<const uint16_t*>(w->W_O), v16, g.D, K, R, static_cast<char*>(ws) + v_bytes, y,
-                (flags & TPLA_DECODE_ACCUMULATE) != 0, out16, s, chunk * kc, kc);
+                (flags & TPLA_DECODE_ACCUMULATE) != 0, out16, s, chunk * kc, kc, ar);
   if (e != cudaSuccess) return cuda_fail(e, "K5b W_O (tcgen05)");
-  if (comm) {                                                      // C1: O = AllReduce(Σ Õ)
+  if (comm && !ar) {                                               // C1: O = AllReduce(Σ Õ)
     ncclResult_t r = g_nccl.AllReduce(y, y, size_t(R) * g.D, ncclFloat32, ncclSum, comm->comm, s);
     if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
     if (out) {
@@ -1018,8 +1062,61 @@ tpla_status tpla_comm_init(tpla_comm** out, const void* unique_id128, int32_t wo
   return ok();
 }
 
+tpla_status tpla_comm_enable_fused_allreduce(tpla_comm* comm, int64_t max_elems) {
+  if (!comm || max_elems < 1) return fail(TPLA_ERR_INVALID_ARG, "bad arguments");
+  if (!load_nccl()) return fail(TPLA_ERR_NCCL, "NCCL not loadable");
+  if (!g_nccl.device_api)
+    return fail(TPLA_ERR_UNSUPPORTED, "the loaded NCCL has no device API matching %d (symmetric windows, LSA barriers)",
+                NCCL_VERSION_CODE);
+  if (comm->ar.window) return ok();
+  const size_t bytes = 2 * size_t(max_elems) * 4;              // two halves (selected by the barrier epoch)
+  void* buf = nullptr;
+  ncclResult_t r = g_nccl.MemAlloc(&buf, bytes);
+  if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclMemAlloc: %s", g_nccl.GetErrorString(r));
+  TPLA_CUDA(cudaMemset(buf, 0, bytes), "zero symmetric buffer");
+  ncclWindow_t win = nullptr;
+  r = g_nccl.WinRegister(comm->comm, buf, bytes, &win, NCCL_WIN_COLL_SYMMETRIC);   // (collective)
+  if (r != ncclSuccess) {
+    g_nccl.MemFree(buf);
+    return fail(TPLA_ERR_NCCL, "ncclCommWindowRegister: %s", g_nccl.GetErrorString(r));
+  }
+  // LSA barriers for the reduce CTAs; the NVLS multicast (lsaMultimem) when the system offers it
+  const char* env = getenv("TPLA_FUSED_AR");
+  bool want_mm = !(env && strcmp(env, "unicast") == 0);
+  ncclDevCommRequirements_t req{};
+  req.lsaBarrierCount = kArCtas;
+  req.lsaMultimem = want_mm;
+  r = g_nccl.DevCommCreate(comm->comm, &req, &comm->dev);       // (collective)
+  if (r != ncclSuccess && want_mm) {
+    want_mm = false;
+    req.lsaMultimem = false;
+    r = g_nccl.DevCommCreate(comm->comm, &req, &comm->dev);
+  }
+  if (r != ncclSuccess) {
+    g_nccl.WinDeregister(comm->comm, win);
+    g_nccl.MemFree(buf);
+    return fail(TPLA_ERR_NCCL, "ncclDevCommCreate: %s", g_nccl.GetErrorString(r));
+  }
+  comm->sym = buf;
+  comm->win = win;
+  comm->dev_ok = true;
+  comm->ar.dev_comm = &comm->dev;
+  comm->ar.window = win;
+  comm->ar.half_elems = size_t(max_elems);
+  comm->ar.multimem = want_mm && comm->world > 1 ? 1 : 0;
+  return ok();
+}
+
+int32_t tpla_comm_fused_allreduce_mode(const tpla_comm* comm) {
+  if (!comm || !comm->ar.window) return 0;
+  return comm->ar.multimem ? 2 : 1;
+}
+
 tpla_status tpla_comm_destroy(tpla_comm* comm) {
   if (!comm) return ok();
+  if (g_nccl.ok && comm->dev_ok) g_nccl.DevCommDestroy(comm->comm, &comm->dev);
+  if (g_nccl.ok && comm->win) g_nccl.WinDeregister(comm->comm, comm->win);
+  if (g_nccl.ok && comm->sym) g_nccl.MemFree(comm->sym);
   if (g_nccl.ok) g_nccl.CommDestroy(comm->comm);
   delete comm;
   return ok();

@@ -788,3 +788,63 @@ def test_prefill_mla_forward(k, L):
 def test_prefill_mla_forward_kimi_long():
     """Kimi-K2 heads (64), a 1100-token prompt: 9 query tiles, the longest attending to 9 key tiles."""
     prefill_mla_forward_case(dev(), synth.PRESETS["kimi"], 2, 1100, sample=97)
+
+
+# ----------------------------------------------------------------------------- f2(i): fused W^O + all-reduce
+def test_fused_allreduce_world1_bit_identical():
+    """SURVEY f2(i) at world 1 (the only size one GPU can run): the K5 segment reduce writes Õ into the
+    NCCL symmetric window, meets its peers at the LSA barrier and sums the ranks itself.  With one rank
+    the sum is the rank's own rows: y and the bf16 output must be bit-identical to the decode without
+    a communicator — for tpla_decode, for decode_v + project_out, repeatedly (the buffer halves
+    alternate with the barrier epoch) and under CUDA-graph replay."""
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    B, n = 3, 150
+    r = TplaRank(spec_of(dims), k=2, g=2, rank=1, batch=B, max_seq_len=n, device=d)
+    w = synth.gen_weights(dims, 16)
+    r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_HADAMARD, sign_seed=5)
+    ck = bf16_from_bits(np.concatenate([synth.gen_raw_ckv(dims, n, 2, b) for b in range(B)]), d)
+    kp = bf16_from_bits(np.concatenate([synth.gen_kpe(dims, n, 2, b) for b in range(B)]), d)
+    seq = torch.repeat_interleave(torch.arange(B, dtype=torch.int32), n).to(d)
+    pos = torch.arange(n, dtype=torch.int32).repeat(B).to(d)
+    r.append(ck, kp, seq, pos, abi.RMS_SLICED)
+    q, qpe = synth.gen_queries(dims, B, 7)
+    q, qpe = bf16_from_bits(q, d), bf16_from_bits(qpe, d)
+    lens = torch.tensor([n, n - 7, 64], dtype=torch.int32, device=d)
+    y0 = torch.zeros((B, dims.D), dtype=torch.float32, device=d)
+    r.decode(q, qpe, lens, y0)
+    comm = abi.tpla_comm_init(abi.tpla_comm_unique_id(), 1, 0)
+    try:
+        abi.tpla_comm_enable_fused_allreduce(comm, 64 * dims.D)
+    except abi.TplaError as e:
+        abi.tpla_comm_destroy(comm)
+        pytest.skip(f"no NCCL device API: {e}")
+    assert abi.tpla_comm_fused_allreduce_mode(comm) == 1          # (world 1: peer loads, no multicast)
+    n0 = abi.tpla_launch_count()
+    ys = [torch.full_like(y0, float("nan")) for _ in range(3)]
+    outs = [torch.empty((B, dims.D), dtype=torch.bfloat16, device=d) for _ in range(3)]
+    for y, out in zip(ys, outs):
+        r.decode(q, qpe, lens, y, out, comm=comm)
+    torch.cuda.synchronize()
+    for y, out in zip(ys, outs):
+        assert torch.equal(y, y0) and torch.equal(out, y0.to(torch.bfloat16))
+    # decode_v + project_out (the group-shared up-projection) on the same communicator
+    v = torch.empty(r.v_acc_shape(B), dtype=torch.float32, device=d)
+    r.decode_v(q, qpe, lens, v)
+    y1 = torch.full_like(y0, float("nan"))
+    out1 = torch.empty((B, dims.D), dtype=torch.bfloat16, device=d)
+    r.project_out(v, y1, out1, comm=comm)
+    # graph capture: two decodes per replay, replayed twice (the epoch parity keeps alternating)
+    yg = [torch.zeros_like(y0) for _ in range(2)]
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+        for y in yg:
+            r.decode(q, qpe, lens, y, comm=comm)
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    abi.tpla_comm_destroy(comm)
+    assert torch.equal(y1, y0) and torch.equal(out1, y0.to(torch.bfloat16))
+    for y in yg:
+        assert torch.equal(y, y0)
+    assert abi.tpla_launch_count() > n0
