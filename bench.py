@@ -79,6 +79,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
     p.add_argument("--batch", type=int, default=None, help="override the workload batch (sweep)")
     p.add_argument("--seq-len", type=int, default=None, help="override the workload context length (sweep)")
+    p.add_argument("--g", type=int, default=None, help="override the workload's latent groups g (sweep)")
+    p.add_argument("--k", type=int, default=None, help="override the workload's TP ranks k (sweep)")
     p.add_argument("--no-graph", action="store_true", help="issue the timed steps eagerly instead of a CUDA graph")
     p.add_argument("--wo", default="auto", choices=["auto", "rank", "shared"],
                    help="up-projection: 'rank' = every rank multiplies its own v_j by its W^O rows (P:139-141); "
@@ -365,6 +367,11 @@ def main():
         wl["B"] = args.batch
     if args.seq_len:
         wl["S"] = args.seq_len
+    if args.g:
+        wl["g"] = args.g
+        wl["xform"] = "hadamard" if args.g > 1 else "identity"
+    if args.k:
+        wl["k"] = args.k
     N = args.gpus
     world = int(os.environ.get("WORLD_SIZE", "1"))
     proc = int(os.environ.get("RANK", "0"))
