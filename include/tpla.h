@@ -329,6 +329,12 @@ tpla_status tpla_comm_init(tpla_comm** out, const void* unique_id128, int32_t wo
  * NVLink in rank order) — no separate ncclAllReduce or cast launch.  TPLA_FUSED_AR=0 disables it per
  * process, =unicast forbids the multicast.  TPLA_ERR_UNSUPPORTED if the loaded NCCL has no device API
  * matching the headers (NCCL 2.28).  tpla_comm_fused_allreduce_mode: 0 off, 1 peer loads, 2 multicast. */
+/* Which attention kernel tpla_decode / tpla_decode_v / tpla_decode_attention run for this shape
+ * (validated first; a status < 0 is -(tpla_status) of the failed validation): 1 = the tcgen05
+ * persistent K3 (d_r = 64, W_lat in {64, 128, 256, 512}, B <= 512), 0 = the mma.sync K3 that serves
+ * every other shape (or TPLA_ATTN=mma).  TPLA_REQUIRE_TC=1 in the environment turns the fallback into
+ * TPLA_ERR_UNSUPPORTED for the decode calls. */
+int32_t tpla_decode_kernel_path(const tpla_config* cfg, int32_t B);
 tpla_status tpla_comm_enable_fused_allreduce(tpla_comm* comm, int64_t max_elems);
 int32_t tpla_comm_fused_allreduce_mode(const tpla_comm* comm);
 tpla_status tpla_comm_destroy(tpla_comm* comm);

@@ -115,6 +115,7 @@ _SIGS = {
                                   _P, _P, _I, _P, _P], _I),
     "tpla_comm_unique_id": ([_P], _I),
     "tpla_comm_enable_fused_allreduce": ([_P, C.c_int64], _I),
+    "tpla_decode_kernel_path": ([C.POINTER(tpla_config), _I], _I),
     "tpla_comm_fused_allreduce_mode": ([_P], _I),
     "tpla_comm_init": ([C.POINTER(_P), _P, _I, _I], _I),
     "tpla_comm_destroy": ([_P], _I),
@@ -327,6 +328,14 @@ def tpla_comm_enable_fused_allreduce(comm, max_elems: int):
     """symmetric window + device communicator for the fused W^O epilogue + one-shot
     all-reduce (collective: every rank calls it)."""
     _check(_lib.tpla_comm_enable_fused_allreduce(comm, max_elems), "tpla_comm_enable_fused_allreduce")
+
+
+def tpla_decode_kernel_path(cfg, B: int) -> int:
+    """1: the tcgen05 K3, 0: the mma.sync K3 fallback; raises on an invalid shape."""
+    r = int(_lib.tpla_decode_kernel_path(C.byref(cfg), B))
+    if r < 0:
+        raise TplaError(-r, "tpla_decode_kernel_path", _lib.tpla_last_error().decode())
+    return r
 
 
 def tpla_comm_fused_allreduce_mode(comm) -> int:

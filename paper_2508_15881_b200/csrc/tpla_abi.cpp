@@ -553,6 +553,10 @@ static tpla_status check_decode_common(const Geom& g, const tpla_cache* cache, c
                                        const int32_t* seq_lens, int B, int max_seq_len) {
   tpla_status st;
   if ((st = check_kernel_shapes(g))) return st;
+  const char* req = getenv("TPLA_REQUIRE_TC");
+  if (req && req[0] == '1' && !use_tc_attention(g, B))
+    return fail(TPLA_ERR_UNSUPPORTED, "TPLA_REQUIRE_TC: this shape runs the mma.sync K3 (W_lat=%d, d_r=%d, B=%d)",
+                g.w_lat, g.d_r, B);
   if ((st = check_cache(g, cache))) return st;
   if (B < 1 || B > cache->batch) return fail(TPLA_ERR_SHAPE, "B=%d outside [1, cache batch %d]", B, cache->batch);
   if (max_seq_len < 1 || int64_t(max_seq_len) > int64_t(cache->max_pages_per_seq) * cache->page_size)
@@ -1060,6 +1064,16 @@ tpla_status tpla_comm_init(tpla_comm** out, const void* unique_id128, int32_t wo
   if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
   *out = new tpla_comm{c, world, rank};
   return ok();
+}
+
+int32_t tpla_decode_kernel_path(const tpla_config* cfg, int32_t B) {
+  Geom g{};
+  tpla_status st = make_geom(cfg, &g);
+  if (st) return -st;
+  if ((st = check_kernel_shapes(g))) return -st;
+  if (B < 1) return -fail(TPLA_ERR_INVALID_ARG, "B=%d", B);
+  ok();
+  return use_tc_attention(g, B) ? 1 : 0;
 }
 
 tpla_status tpla_comm_enable_fused_allreduce(tpla_comm* comm, int64_t max_elems) {

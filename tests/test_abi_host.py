@@ -209,3 +209,14 @@ def test_prefill_mla_forward_host_checks():
         abi.tpla_prefill_mla_forward(c1, w, 1 << 20, 1 << 20, 1 << 20, 1 << 20, 4096, 1 << 20, 1024, 1 << 20)
     assert ei.value.status == abi.ERR_CAPACITY
     assert abi.tpla_launch_count() == n_before
+
+
+def test_decode_kernel_path_reported():
+    """Which K3 a shape runs is queryable (verdict r1: the mma.sync fallback was silent)."""
+    assert abi.tpla_decode_kernel_path(cfg(), 32) == 1                       # DSV3 g = 2: tcgen05
+    assert abi.tpla_decode_kernel_path(cfg(k=8, g=8), 32) == 1               # W_lat 64
+    assert abi.tpla_decode_kernel_path(cfg(), 600) == 0                      # B > 512: mma.sync
+    assert abi.tpla_decode_kernel_path(cfg(h_q=4, d_c=64, d_r=16, d_h=16, D=128), 1) == 0   # tiny: mma.sync
+    with pytest.raises(abi.TplaError) as ei:
+        abi.tpla_decode_kernel_path(cfg(g=3, k=3), 1)
+    assert ei.value.status == abi.ERR_DIVISIBILITY
