@@ -88,9 +88,12 @@ def parse():
                         "across processes (SURVEY f2(ii)); auto = shared when g > 1")
     p.add_argument("--no-fused-ar", action="store_true",
                    help="N > 1: plain ncclAllReduce after the W^O GEMM instead of the fused one-shot all-reduce")
-    p.add_argument("--no-rank-streams", action="store_true",
-                   help="issue the co-located ranks of a latent group serially on one stream (default: one stream "
-                        "per rank, separate v accumulators summed in tpla_project_out_sum)")
+    p.add_argument("--rank-streams", default="auto", choices=["auto", "off", "full", "pre"],
+                   help="co-located ranks of a latent group: off = serially on one stream; full = one stream per rank "
+                        "(separate v accumulators summed in tpla_project_out_sum); pre = each rank's K1 / K3p / K2 on "
+                        "its own stream, the attention stages (K3, K45) in rank order on the main stream; auto = pre "
+                        "with 2 ranks per group, full with more")
+    p.add_argument("--no-rank-streams", action="store_true", help="= --rank-streams off")
     p.add_argument("--profile-region", action="store_true",
                    help="cudaProfilerStart/Stop around the timed region (for ncu --profile-from-start off)")
     return p.parse_args()
@@ -455,8 +458,10 @@ def main():
     # stream into its own accumulator (the ranks are independent devices in the deployment),
     # summed in rank order by tpla_project_out_sum.  Groups spanning processes keep the in-place sum
     # that the reduce-scatter needs.
-    par = [wo == "shared" and not args.no_rank_streams and gcomms.get(grp.procs) is None and len(grp.local_ranks) > 1
+    rs_mode = "off" if args.no_rank_streams else args.rank_streams
+    par = [wo == "shared" and rs_mode != "off" and gcomms.get(grp.procs) is None and len(grp.local_ranks) > 1
            for grp in groups]
+    par_mode = [("pre" if len(grp.local_ranks) == 2 else "full") if rs_mode == "auto" else rs_mode for grp in groups]
     v_sep = [[torch.zeros_like(v_acc[gi]) for _ in grp.local_ranks] if par[gi] else None
              for gi, grp in enumerate(groups)]
     rank_streams = {r: torch.cuda.Stream(device=dev) for gi, grp in enumerate(groups) if par[gi] for r in grp.local_ranks}
@@ -471,7 +476,7 @@ def main():
         if wo == "shared":
             main = torch.cuda.current_stream()
             for gi, (grp, va) in enumerate(zip(groups, v_acc)):
-                if par[gi] and not serial:                 # one stream per co-located rank
+                if par[gi] and not serial and par_mode[gi] == "full":     # one stream per co-located rank
                     for j, r in enumerate(grp.local_ranks):
                         st = rank_streams[r]
                         st.wait_stream(main)
@@ -480,6 +485,16 @@ def main():
                             by_id[r].decode_v(q, qq, seq_lens, v_sep[gi][j], n_chunks=grp.n_chunks)
                     for r in grp.local_ranks:
                         main.wait_stream(rank_streams[r])
+                elif par[gi] and not serial:               # the query stages early, the attention in order
+                    for j, r in enumerate(grp.local_ranks):
+                        st = rank_streams[r]
+                        st.wait_stream(main)
+                        with torch.cuda.stream(st):
+                            by_id[r].append(ck, kp, seq_idx, pos_new, abi.RMS_SLICED)
+                            by_id[r].decode_v(q, qq, seq_lens, v_sep[gi][j], n_chunks=grp.n_chunks, stage="pre")
+                    for j, r in enumerate(grp.local_ranks):
+                        main.wait_stream(rank_streams[r])
+                        by_id[r].decode_v(q, qq, seq_lens, v_sep[gi][j], n_chunks=grp.n_chunks, stage="attn")
                 else:
                     for j, r in enumerate(grp.local_ranks):
                         by_id[r].append(ck, kp, seq_idx, pos_new, abi.RMS_SLICED)
@@ -773,7 +788,8 @@ def main():
                 "roofline": roofline, "headline": headline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "gpu_launches_per_step": launches / args.steps, "clocks": clk, "clocks_sustained": clocks_sust,
                 "kernels": kernels,
-                "cuda_graph": graph is not None, "rank_streams": any(par),
+                "cuda_graph": graph is not None,
+                "rank_streams": sorted({m for m, p in zip(par_mode, par) if p}) or "off",
                 "all_reduce": ({0: "ncclAllReduce", 1: "fused into the K5 reduce (LSA peer loads)",
                                 2: "fused into the K5 reduce (NVLS multimem.ld_reduce)"}[ar_mode]
                                if N > 1 else "none (N = 1)"),

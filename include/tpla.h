@@ -67,7 +67,12 @@ enum {
 
 /* tpla_decode flags */
 enum {
-  TPLA_DECODE_ACCUMULATE = 1  /* y += Õ_j instead of y = Õ_j (single-GPU k-shard emulation) */
+  TPLA_DECODE_ACCUMULATE = 1,  /* y += Õ_j instead of y = Õ_j (single-GPU k-shard emulation)          */
+  /* tpla_decode_v in two calls on the same workspace (a scheduler may issue the first early, on
+   * another stream): STAGE_PRE = K3p + K2 only (the schedule and Q'_j), STAGE_ATTN = K3 + K4/K5a only
+   * (requires the STAGE_PRE call with the same inputs to have completed).  Neither bit: both. */
+  TPLA_DECODE_STAGE_PRE = 2,
+  TPLA_DECODE_STAGE_ATTN = 4
 };
 
 /* Model + deployment.  Semantics: PAPER.md §3.1/§3.3 symbols; k devices, g latent groups (§4.4). */
@@ -277,6 +282,7 @@ tpla_status tpla_prefill_mla_forward(const tpla_config* cfg, const tpla_prefill_
  * element (row, col) at ((col / kc) * B*n_q + row) * kc + col % kc, kc = K / n_chunks (64 * n_chunks | K).
  *   tpla_decode_v:    K2, K3, K4+K5a of this device into v_acc (= v_j, or += with TPLA_DECODE_ACCUMULATE).
  *                     Needs the tcgen05 attention path; same inputs and workspace as tpla_decode_mtp.
+ *                     TPLA_DECODE_STAGE_PRE / _ATTN split it into its query stage and attention stage.
  *   tpla_project_out: with group_comm (world n_chunks, rank chunk): in-place ncclReduceScatter of v_acc
  *                     (sum over the group; chunk `chunk` lands in place), then for every caller
  *                     y [R, D] fp32 (=, or += with TPLA_DECODE_ACCUMULATE) = bf16(v_acc chunk) ·

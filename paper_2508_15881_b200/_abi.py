@@ -36,6 +36,7 @@ OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_DIVISIBILITY, ERR_CAPACITY, ERR_CUDA, ERR_NC
 XFORM_IDENTITY, XFORM_HADAMARD, XFORM_PCA = 0, 1, 2
 RMS_SLICED, RMS_EXACT, RMS_NONE = 0, 1, 2
 DECODE_ACCUMULATE = 1
+DECODE_STAGE_PRE, DECODE_STAGE_ATTN = 2, 4
 
 _STATUS = {0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "DIVISIBILITY", 4: "CAPACITY", 5: "CUDA", 6: "NCCL",
            7: "UNSUPPORTED"}

@@ -781,12 +781,17 @@ tpla_status tpla_decode_v(const tpla_config* cfg, const tpla_weights* w, const t
   auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
   const auto* qn = static_cast<const uint16_t*>(q_nope);
   auto* plan = reinterpret_cast<int32_t*>(base + L.plan);
-  cudaError_t e = launch_attn_plan(g, *cache, seq_lens, B, L.n_cta, plan, s);   // K3p, ahead of K2
-  if (e != cudaSuccess) return cuda_fail(e, "K3p plan");
-  e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK),
-                                   qn + size_t(g.head_begin) * g.d_h, long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h,
-                                   B * n_q, q_lat, true, s);
-  if (e != cudaSuccess) return cuda_fail(e, "K2 absorb_q");
+  const bool pre = !(flags & TPLA_DECODE_STAGE_ATTN), attn = !(flags & TPLA_DECODE_STAGE_PRE);
+  if (!pre && !attn) return fail(TPLA_ERR_INVALID_ARG, "STAGE_PRE and STAGE_ATTN together");
+  cudaError_t e = cudaSuccess;
+  if (pre) {
+    e = launch_attn_plan(g, *cache, seq_lens, B, L.n_cta, plan, s);   // K3p, ahead of K2
+    if (e != cudaSuccess) return cuda_fail(e, "K3p plan");
+    e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK), qn + size_t(g.head_begin) * g.d_h,
+                         long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h, B * n_q, q_lat, true, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K2 absorb_q");
+  }
+  if (!attn) return ok();
   e = launch_decode_attn_tc(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, n_q, L.n_cta, plan,
                             o_part, ml_part, meta, s);
   if (e != cudaSuccess) return cuda_fail(e, "K3 decode attention");

@@ -179,13 +179,16 @@ class TplaRank:
                             self.ws, self.ws_bytes, y, out, abi.DECODE_ACCUMULATE if accumulate else 0, comm,
                             stream_ptr(stream))
 
-    def decode_v(self, q_nope, q_pe, seq_lens, v_acc, *, n_chunks=1, accumulate=False, stream=None):
+    def decode_v(self, q_nope, q_pe, seq_lens, v_acc, *, n_chunks=1, accumulate=False, stage=None, stream=None):
         """K2..K5a into v_acc fp32 [n_chunks, B * n_q, H_loc * d_h / n_chunks] (f2(ii): the latent group
-        sums v and shares one W^O read).  q_nope [B, h_q, d_h] or [B, n_q, h_q, d_h]."""
+        sums v and shares one W^O read).  q_nope [B, h_q, d_h] or [B, n_q, h_q, d_h].
+        stage: None (all), "pre" (K3p + K2 only) or "attn" (K3 + K45, after a "pre" call)."""
         B = int(q_nope.shape[0])
         n_q = int(q_nope.shape[1]) if q_nope.dim() == 4 else 1
+        flags = (abi.DECODE_ACCUMULATE if accumulate else 0) | {None: 0, "pre": abi.DECODE_STAGE_PRE,
+                                                                 "attn": abi.DECODE_STAGE_ATTN}[stage]
         abi.tpla_decode_v(self.cfg, self.weights, self.cache, q_nope, q_pe, seq_lens, B, n_q, self.max_seq_len, self.ws,
-                          self.ws_bytes, v_acc, n_chunks, abi.DECODE_ACCUMULATE if accumulate else 0, stream_ptr(stream))
+                          self.ws_bytes, v_acc, n_chunks, flags, stream_ptr(stream))
 
     def v_acc_shape(self, rows: int, n_chunks: int = 1):
         return (n_chunks, rows, self.plan.h_loc * self.spec.d_h // n_chunks)

@@ -848,3 +848,34 @@ def test_fused_allreduce_world1_bit_identical():
     for y in yg:
         assert torch.equal(y, y0)
     assert abi.tpla_launch_count() > n0
+
+
+def test_decode_v_two_stages_bit_identical():
+    """tpla_decode_v in two calls (STAGE_PRE: K3p + K2, then STAGE_ATTN: K3 + K45, as bench.py schedules
+    co-located ranks) gives the same bits as the one-call decode_v; both flags together are rejected."""
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    B, n = 3, 300
+    for k, g in ((2, 2), (8, 8)):
+        r = TplaRank(spec_of(dims), k=k, g=g, rank=k - 1, batch=B, max_seq_len=n, device=d)
+        w = synth.gen_weights(dims, 17)
+        r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=abi.XFORM_HADAMARD, sign_seed=5)
+        ck = bf16_from_bits(np.concatenate([synth.gen_raw_ckv(dims, n, 2, b) for b in range(B)]), d)
+        kp = bf16_from_bits(np.concatenate([synth.gen_kpe(dims, n, 2, b) for b in range(B)]), d)
+        seq = torch.repeat_interleave(torch.arange(B, dtype=torch.int32), n).to(d)
+        pos = torch.arange(n, dtype=torch.int32).repeat(B).to(d)
+        r.append(ck, kp, seq, pos, abi.RMS_SLICED)
+        q, qpe = synth.gen_queries(dims, B, 7)
+        q, qpe = bf16_from_bits(q, d), bf16_from_bits(qpe, d)
+        lens = torch.tensor([n, n - 7, 64], dtype=torch.int32, device=d)
+        v0 = torch.zeros(r.v_acc_shape(B), dtype=torch.float32, device=d)
+        v1 = torch.full_like(v0, float("nan"))
+        r.decode_v(q, qpe, lens, v0)
+        r.decode_v(q, qpe, lens, v1, stage="pre")
+        r.decode_v(q, qpe, lens, v1, stage="attn")
+        torch.cuda.synchronize()
+        assert torch.equal(v0, v1)
+        with pytest.raises(abi.TplaError) as ei:
+            abi.tpla_decode_v(r.cfg, r.weights, r.cache, q, qpe, lens, B, 1, r.max_seq_len, r.ws, r.ws_bytes, v1, 1,
+                              abi.DECODE_STAGE_PRE | abi.DECODE_STAGE_ATTN, 0)
+        assert ei.value.status == abi.ERR_INVALID_ARG
