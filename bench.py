@@ -91,8 +91,8 @@ def parse():
     p.add_argument("--rank-streams", default="auto", choices=["auto", "off", "full", "pre"],
                    help="co-located ranks of a latent group: off = serially on one stream; full = one stream per rank "
                         "(separate v accumulators summed in tpla_project_out_sum); pre = each rank's K1 / K3p / K2 on "
-                        "its own stream, the attention stages (K3, K45) in rank order on the main stream; auto = pre "
-                        "with 2 ranks per group, full with more")
+                        "its own stream, the attention stages (K3, K45) in rank order on the main stream; auto = full "
+                        "for groups of more than 2 ranks, off otherwise")
     p.add_argument("--no-rank-streams", action="store_true", help="= --rank-streams off")
     p.add_argument("--profile-region", action="store_true",
                    help="cudaProfilerStart/Stop around the timed region (for ncu --profile-from-start off)")
@@ -461,7 +461,10 @@ def main():
     rs_mode = "off" if args.no_rank_streams else args.rank_streams
     par = [wo == "shared" and rs_mode != "off" and gcomms.get(grp.procs) is None and len(grp.local_ranks) > 1
            for grp in groups]
-    par_mode = [("pre" if len(grp.local_ranks) == 2 else "full") if rs_mode == "auto" else rs_mode for grp in groups]
+    # auto: one stream per rank for groups of more than two ranks (h8 666 -> 586 us, c3 / c2 a few %);
+    # two ranks (c1) gain nothing from either overlap (A/B: off 344-348, pre 349, full 347-352 us)
+    par = [p and (rs_mode != "auto" or len(grp.local_ranks) > 2) for p, grp in zip(par, groups)]
+    par_mode = ["full" if rs_mode == "auto" else rs_mode for grp in groups]
     v_sep = [[torch.zeros_like(v_acc[gi]) for _ in grp.local_ranks] if par[gi] else None
              for gi, grp in enumerate(groups)]
     rank_streams = {r: torch.cuda.Stream(device=dev) for gi, grp in enumerate(groups) if par[gi] for r in grp.local_ranks}
