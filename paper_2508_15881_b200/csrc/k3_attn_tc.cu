@@ -229,12 +229,17 @@ __device__ __forceinline__ int block_excl_scan(int x, int* wsum, int& total) {  
   return r;
 }
 
-// One CTA (512 threads) computes the schedule of every K3 CTA: the flattened (sequence, tile) list
-// cut into equal work ranges with a per-sequence header cost (tile_of), each CTA's first segment id,
-// and its first 32 box rows through the page table.  It reads only caller inputs, so it runs under
-// the predecessor's tail (K1) and waits only before its stores.
+// K3p: CTA 0 computes every K3 CTA's schedule entry (the flattened (sequence, tile) list cut into
+// equal work ranges with a per-sequence header cost, tile_of; each CTA's first segment id by a block
+// scan) and copies the sequence scan; CTAs 1.. each resolve the first 32 box rows of 8 K3 CTAs through
+// the page table, one lookup per thread (each recomputes the scan: B <= 512 lengths, one per thread).
+// (One CTA doing all 148 x 32 lookups took ~16 us, measured: its dependent loads did not overlap.)
+// Reads only caller inputs: runs under the predecessor's tail and waits only before its stores.
+constexpr int kPlanThreads = 512;
+constexpr int kPlanRowCtas = kPlanThreads / 32;           // K3 CTAs whose rows one plan CTA resolves
+
 template <int W_LAT>
-__global__ void __launch_bounds__(512) attn_plan_kernel(PlanArgs p) {
+__global__ void __launch_bounds__(kPlanThreads) attn_plan_kernel(PlanArgs p) {
   pdl_trigger();
   using C = Cfg<W_LAT>;
   __shared__ int cum[kMaxB + 1], slen[kMaxB], lo_arr[kMaxCta + 1], wsum[40];
@@ -248,51 +253,46 @@ __global__ void __launch_bounds__(512) attn_plan_kernel(PlanArgs p) {
   __syncthreads();
   const int n = p.n_cta;
   const long Wt = long(total) + long(C::SEQ_COST) * p.B;            // total work units
-  for (int cc = tid; cc <= n; cc += 512) lo_arr[cc] = tile_of<C::SEQ_COST>(cum, p.B, cc * Wt / n);
-  __syncthreads();
-  int lo = 0, hi = 0, bf = 0, bl = -1;
-  if (tid < n) {
-    lo = lo_arr[tid];
-    hi = lo_arr[tid + 1];
-    if (lo < hi) {
-      bf = upper_bound_cum(cum, p.B + 1, lo) - 1;
-      bl = upper_bound_cum(cum, p.B + 1, hi - 1) - 1;
-    }
-  }
-  int n_seg_total;
-  const int seg_base = block_excl_scan(tid < n ? bl - bf + 1 : 0, wsum, n_seg_total);
-  // first 32 box rows of every CTA (the producer's first batch), resolved before the wait
-  constexpr int kPer = kMaxCta * 32 / 512;
-  int rows[kPer];
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const int idx = tid + i * 512, cc = idx >> 5, u = idx & 31;
-    rows[i] = 0;
-    if (cc < n) {
-      const int tt = lo_arr[cc] + u / C::SUB;
-      if (tt < lo_arr[cc + 1]) {
-        const int bb = upper_bound_cum(cum, p.B + 1, tt) - 1;
-        const int tok0 = (tt - cum[bb]) * C::TT;
-        int tok = tok0 + (u % C::SUB) * kSub;
-        if (tok >= slen[bb]) tok = tok0;
-        rows[i] = p.block_table[(long)bb * p.max_pages + tok / p.page_size] * p.page_size + tok % p.page_size;
+  if (blockIdx.x == 0) {
+    for (int cc = tid; cc <= n; cc += kPlanThreads) lo_arr[cc] = tile_of<C::SEQ_COST>(cum, p.B, cc * Wt / n);
+    __syncthreads();
+    int lo = 0, hi = 0, bf = 0, bl = -1;
+    if (tid < n) {
+      lo = lo_arr[tid];
+      hi = lo_arr[tid + 1];
+      if (lo < hi) {
+        bf = upper_bound_cum(cum, p.B + 1, lo) - 1;
+        bl = upper_bound_cum(cum, p.B + 1, hi - 1) - 1;
       }
     }
+    int n_seg_total;
+    const int seg_base = block_excl_scan(tid < n ? bl - bf + 1 : 0, wsum, n_seg_total);
+    pdl_wait();   // first store: the previous launch's K3 read this plan (write-after-read)
+    if (tid < n) {
+      int32_t* e = p.plan + tid * kPlanStride;
+      e[0] = lo; e[1] = hi; e[2] = bf; e[3] = bl; e[4] = seg_base;
+    }
+    int32_t* pc = p.plan + n * kPlanStride;
+    for (int i = tid; i <= p.B; i += kPlanThreads) pc[i] = cum[i];
+    for (int i = tid; i < p.B; i += kPlanThreads) pc[p.B + 1 + i] = slen[i];
+    return;
   }
-  pdl_wait();   // first store: the previous launch's K3 read this plan (write-after-read)
-  if (tid < n) {
-    int32_t* e = p.plan + tid * kPlanStride;
-    e[0] = lo; e[1] = hi; e[2] = bf; e[3] = bl; e[4] = seg_base;
+  // first 32 box rows of K3 CTAs [c0, c0 + kPlanRowCtas)
+  const int c0 = (blockIdx.x - 1) * kPlanRowCtas, cc = c0 + tid / 32, u = tid & 31;
+  int row = 0;
+  if (cc < n) {
+    const int lo = tile_of<C::SEQ_COST>(cum, p.B, cc * Wt / n), hi = tile_of<C::SEQ_COST>(cum, p.B, (cc + 1) * Wt / n);
+    const int tt = lo + u / C::SUB;
+    if (tt < hi) {
+      const int bb = upper_bound_cum(cum, p.B + 1, tt) - 1;
+      const int tok0 = (tt - cum[bb]) * C::TT;
+      int tok = tok0 + (u % C::SUB) * kSub;
+      if (tok >= slen[bb]) tok = tok0;
+      row = p.block_table[(long)bb * p.max_pages + tok / p.page_size] * p.page_size + tok % p.page_size;
+    }
   }
-  int32_t* pc = p.plan + n * kPlanStride;
-  for (int i = tid; i <= p.B; i += 512) pc[i] = cum[i];
-  for (int i = tid; i < p.B; i += 512) pc[p.B + 1 + i] = slen[i];
-  int32_t* pr = pc + 2 * p.B + 1;
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const int idx = tid + i * 512;
-    if ((idx >> 5) < n) pr[idx] = rows[i];
-  }
+  pdl_wait();
+  if (cc < n) p.plan[n * kPlanStride + 2 * p.B + 1 + cc * 32 + u] = row;
 }
 
 // MODE 0: the kernel.  MODE 1 (diagnostic, TPLA_K3_MODE=stream): the TMA ring alone — every
@@ -1223,7 +1223,7 @@ size_t attn_plan_bytes(int n_cta, int B) {
 template <int W_LAT>
 cudaError_t launch_plan_w(const PlanArgs& p, cudaStream_t s) {
   KernelScope ks("K3p_attn_plan", s);
-  return launch_k(attn_plan_kernel<W_LAT>, 1, 512, 0, s, p);
+  return launch_k(attn_plan_kernel<W_LAT>, 1 + (p.n_cta + kPlanRowCtas - 1) / kPlanRowCtas, kPlanThreads, 0, s, p);
 }
 
 cudaError_t launch_attn_plan(const Geom& g, const tpla_cache& cache, const int32_t* seq_lens, int B, int n_cta,
