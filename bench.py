@@ -461,9 +461,11 @@ def main():
     rs_mode = "off" if args.no_rank_streams else args.rank_streams
     par = [wo == "shared" and rs_mode != "off" and gcomms.get(grp.procs) is None and len(grp.local_ranks) > 1
            for grp in groups]
-    # auto: one stream per rank for groups of more than two ranks (h8 666 -> 586 us, c3 / c2 a few %);
-    # two ranks (c1) gain nothing from either overlap (A/B: off 344-348, pre 349, full 347-352 us)
-    par = [p and (rs_mode != "auto" or len(grp.local_ranks) > 2) for p, grp in zip(par, groups)]
+    # auto: one stream per rank for groups of more than two ranks (h8 666 -> 586 us, c3 / c2 a few %) or
+    # when a rank's attention is short (batch 1 at 32K: 155 -> 125 us); two ranks with long K3s (c1)
+    # gain nothing from either overlap (A/B: off 344-348, pre 349, full 347-352 us)
+    short_k3 = B * S * (dims.d_c // g + dims.d_r) * 2 < (128 << 20)
+    par = [p and (rs_mode != "auto" or len(grp.local_ranks) > 2 or short_k3) for p, grp in zip(par, groups)]
     par_mode = ["full" if rs_mode == "auto" else rs_mode for grp in groups]
     v_sep = [[torch.zeros_like(v_acc[gi]) for _ in grp.local_ranks] if par[gi] else None
              for gi, grp in enumerate(groups)]
