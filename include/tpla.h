@@ -181,6 +181,17 @@ tpla_status tpla_append_kv(const tpla_config* cfg, const tpla_weights* w, const 
 /* PD-separated prefill: the prompt rows are written to this device's
  * cache with the EXACT (unsliced) RMS, so decode reuses the MLA prefill cache.  q must be NULL:
  * the causal prefill attention is tpla_prefill_attention (returns TPLA_ERR_UNSUPPORTED otherwise). */
+/* "Norm only" rows (Fig. 3 "TPLA (norm only)"): the ablation where the
+ * RMSNorm is sliced but the softmax is not.  On one device holding the whole latent (cfg.g = 1), each
+ * row c' = c U is cut into n_slices (1, 2, 4, 8) slices of d_c / n_slices coordinates and slice s is
+ * divided by its own sliced RMS sqrt(alpha[s] / d_c ||c'_s||^2 + eps) (Condition 1 chain);
+ * decoding these rows with the g = 1 kernels and mu = 1 sums the partial logits of the slices before
+ * ONE softmax — exactly the all-gather-the-logits variant of P:469 (oracle tpla_decode_exact_logits).
+ * alpha: host [n_slices].  Otherwise as tpla_append_kv. */
+tpla_status tpla_append_kv_norm_only(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                                     const void* c_kv, const void* k_pe, const int32_t* seq_idx, const int32_t* pos,
+                                     int32_t n, int32_t n_slices, const float* alpha, int32_t* n_dropped,
+                                     void* stream);
 tpla_status tpla_prefill_mla(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
                              const void* c_kv, const void* k_pe, const int32_t* seq_idx, const int32_t* pos,
                              int32_t n, const void* q, void* stream);

@@ -191,14 +191,14 @@ def tpla_decode_step(pb: Problem, k: int, g: int, *, round_rows=None, return_par
     return (o, ys, parts) if return_parts else o
 
 
-def tpla_decode_exact_logits(pb: Problem, g: int):
+def tpla_decode_exact_logits(pb: Problem, g: int, *, round_rows=None):
     """Exact-softmax variant (SURVEY.md pin c10; the all-gather / row-parallel route of
     P:232-236 and the "norm only" ablation): partial NoPE logits of the g shards are
     summed (mu = 1) BEFORE one softmax; RoPE logits added once.  k = g (one device per shard)."""
     d_c, d_r = pb.U.shape[0], pb.k_pe[0].shape[1]
     plans = [make_plan(g, g, pb.h_q, d_c, d_r, r) for r in range(g)]
     dws = [convert_weights(pb.W_UK, pb.W_UV, pb.gamma, pb.W_O, pb.U, pl, 1.0, d_h=pb.d_h) for pl in plans]
-    rows = [device_rows(pb, pl, pb.alpha[pl.shard]) for pl in plans]
+    rows = [device_rows(pb, pl, pb.alpha[pl.shard], round_rows=round_rows) for pl in plans]   # (R19: bf16 cache)
     B = pb.q_nope.shape[0]
     out = np.zeros((B, pb.W_O.shape[1]))
     for b in range(B):

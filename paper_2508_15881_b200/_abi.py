@@ -89,6 +89,8 @@ _SIGS = {
                               C.POINTER(tpla_weights), _P], _I),
     "tpla_append_kv": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _P, _P, _I,
                         _I, _P, _P], _I),
+    "tpla_append_kv_norm_only": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _P,
+                                  _P, _I, _I, _P, _P, _P], _I),
     "tpla_prefill_mla": ([C.POINTER(tpla_config), C.POINTER(tpla_weights), C.POINTER(tpla_cache), _P, _P, _P, _P,
                           _I, _P, _P], _I),
     "tpla_decode_workspace_bytes": ([C.POINTER(tpla_config), _I, _I, C.POINTER(_S)], _I),
@@ -209,6 +211,13 @@ def tpla_convert_weights(cfg, xform_kind, sign_seed, U_pca, alpha, mu, W_UK, W_U
 def tpla_append_kv(cfg, w, cache, c_kv, k_pe, seq_idx, pos, n, rms_mode, n_dropped=None, stream=0):
     _check(_lib.tpla_append_kv(C.byref(cfg), C.byref(w), C.byref(cache), _ptr(c_kv), _ptr(k_pe), _ptr(seq_idx),
                                _ptr(pos), n, rms_mode, _ptr(n_dropped), _ptr(stream)), "tpla_append_kv")
+
+
+def tpla_append_kv_norm_only(cfg, w, cache, c_kv, k_pe, seq_idx, pos, n, alpha, n_dropped=None, stream=0):
+    a = np.ascontiguousarray(alpha, np.float32)
+    _check(_lib.tpla_append_kv_norm_only(C.byref(cfg), C.byref(w), C.byref(cache), _ptr(c_kv), _ptr(k_pe),
+                                         _ptr(seq_idx), _ptr(pos), n, a.size, _ptr(a), _ptr(n_dropped), _ptr(stream)),
+           "tpla_append_kv_norm_only")
 
 
 def tpla_prefill_mla(cfg, w, cache, c_kv, k_pe, seq_idx, pos, n, q=None, stream=0):

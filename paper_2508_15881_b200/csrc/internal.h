@@ -60,10 +60,11 @@ SplitPlan choose_split(int B, int max_seq_len);
 WsLayout ws_layout(const Geom& g, int B, int n_q, int max_seq_len);
 
 // ---- kernels (each returns cudaGetLastError() after launch) ----
+// n_norm > 0: "norm only" rows: the g = 1 row normalised per slice (n_norm slices, alpha_s host)
 cudaError_t launch_append_kv(const Geom& g, int xform_kind, const float* xform, float alpha_j,
                              const tpla_cache& cache, const uint16_t* c_kv, const uint16_t* k_pe,
                              const int32_t* seq_idx, const int32_t* pos, int n, int rms_mode,
-                             int32_t* n_dropped, cudaStream_t s);
+                             int32_t* n_dropped, cudaStream_t s, int n_norm = 0, const float* alpha_s = nullptr);
 
 // out[b, h, r] = sum_c W[h, r, c] * x[b, h, c]     (K2 with R=W_lat,C=d_h; K5a with R=d_h,C=W_lat)
 // x has row stride x_head_stride elements between heads and x_batch_stride between batches.

@@ -16,6 +16,8 @@
 namespace tpla {
 namespace {
 
+constexpr int kMaxNormSlices = 8;
+
 struct AppendArgs {
   const uint16_t* c_kv;
   const uint16_t* k_pe;
@@ -29,6 +31,10 @@ struct AppendArgs {
   int n, d_c, d_r, w_lat, lat_begin, page_size, max_pages, row_stride, batch;
   int xform_kind, rms_mode;
   float alpha, eps;
+  // "norm only": a g = 1 row normalised per slice — n_norm slices of d_c / n_norm
+  // coordinates, slice s divided by sqrt(alpha_s / d_c ||c'_s||^2 + eps); 0 = off
+  int n_norm;
+  float alpha_s[kMaxNormSlices];
 };
 
 template <int E>
@@ -89,12 +95,23 @@ __device__ __forceinline__ void append_row(const AppendArgs& a) {
     __syncwarp();
     // pass 1: slice energy; pass 2 recomputes the projection (keeps registers independent of W)
     float ss = 0.f;
+    float ssn[kMaxNormSlices];                    // norm only: per-slice energies
+#pragma unroll
+    for (int q = 0; q < kMaxNormSlices; ++q) ssn[q] = 0.f;
+    const int wn = a.n_norm > 0 ? W / a.n_norm : W;
     for (int l = lane; l < W; l += 32) {
       float acc = 0.f;
       for (int i = 0; i < a.d_c; ++i) acc = fmaf(c[i], a.xform[(long)i * W + l], acc);
       ss += acc * acc;
+#pragma unroll
+      for (int q = 0; q < kMaxNormSlices; ++q)
+        if (q == l / wn) ssn[q] += acc * acc;
     }
     ss = warp_sum(ss);
+    float rn[kMaxNormSlices];
+#pragma unroll
+    for (int q = 0; q < kMaxNormSlices; ++q)
+      rn[q] = q < a.n_norm ? rsqrtf(a.alpha_s[q] / a.d_c * warp_sum(ssn[q]) + a.eps) : 1.f;
     float r;
     if (a.rms_mode == TPLA_RMS_SLICED) r = rsqrtf(a.alpha / a.d_c * ss + a.eps);
     else if (a.rms_mode == TPLA_RMS_EXACT) r = rsqrtf(ss_full / a.d_c + a.eps);
@@ -103,7 +120,11 @@ __device__ __forceinline__ void append_row(const AppendArgs& a) {
     for (int l = lane; l < W; l += 32) {
       float acc = 0.f;
       for (int i = 0; i < a.d_c; ++i) acc = fmaf(c[i], a.xform[(long)i * W + l], acc);
-      dst[l] = f2bf(acc * r);
+      float rr = r;
+#pragma unroll
+      for (int q = 0; q < kMaxNormSlices; ++q)
+        if (a.n_norm > 0 && q == l / wn) rr = rn[q];
+      dst[l] = f2bf(acc * rr);
     }
   } else {
     if (a.xform_kind == TPLA_XFORM_HADAMARD) {
@@ -135,11 +156,17 @@ __device__ __forceinline__ void append_row(const AppendArgs& a) {
 #pragma unroll
       for (int i = 0; i < E; ++i) ss += x[i] * x[i];
     }
-    ss = warp_sum(ss);
     float r;
-    if (a.rms_mode == TPLA_RMS_SLICED) r = rsqrtf(a.alpha / a.d_c * ss + a.eps);
-    else if (a.rms_mode == TPLA_RMS_EXACT) r = rsqrtf(ss_full / a.d_c + a.eps);
-    else r = 1.f;
+    if (a.n_norm > 0) {                           // norm only: each slice's lanes reduce among themselves
+      const int lanes = 32 / a.n_norm;            // (a power of two: aligned xor groups)
+      for (int m = 1; m < lanes; m <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
+      r = rsqrtf(a.alpha_s[lane / lanes] / a.d_c * ss + a.eps);
+    } else {
+      ss = warp_sum(ss);
+      if (a.rms_mode == TPLA_RMS_SLICED) r = rsqrtf(a.alpha / a.d_c * ss + a.eps);
+      else if (a.rms_mode == TPLA_RMS_EXACT) r = rsqrtf(ss_full / a.d_c + a.eps);
+      else r = 1.f;
+    }
     pdl_wait();   // first store: the previous step's K3 may still read this row's 64-row box
     if (mine) {
       uint16_t* o = dst + (e0 - a.lat_begin);
@@ -177,8 +204,10 @@ cudaError_t launch_E(const AppendArgs& a, cudaStream_t s) {
 cudaError_t launch_append_kv(const Geom& g, int xform_kind, const float* xform, float alpha_j,
                              const tpla_cache& cache, const uint16_t* c_kv, const uint16_t* k_pe,
                              const int32_t* seq_idx, const int32_t* pos, int n, int rms_mode,
-                             int32_t* n_dropped, cudaStream_t s) {
+                             int32_t* n_dropped, cudaStream_t s, int n_norm, const float* alpha_s) {
   AppendArgs a;
+  a.n_norm = n_norm;
+  for (int q = 0; q < kMaxNormSlices; ++q) a.alpha_s[q] = (n_norm > 0 && q < n_norm) ? alpha_s[q] : 1.f;
   a.c_kv = c_kv; a.k_pe = k_pe; a.seq_idx = seq_idx; a.pos = pos; a.xform = xform;
   a.base = static_cast<uint16_t*>(cache.base); a.block_table = cache.block_table; a.n_dropped = n_dropped;
   a.num_pages = cache.num_pages; a.n = n; a.d_c = g.d_c; a.d_r = g.d_r; a.w_lat = g.w_lat;

@@ -493,7 +493,8 @@ tpla_status tpla_convert_weights(const tpla_config* cfg, int32_t xform_kind, uin
 
 static tpla_status append_common(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
                                  const void* c_kv, const void* k_pe, const int32_t* seq_idx, const int32_t* pos,
-                                 int32_t n, int32_t rms_mode, int32_t* n_dropped, void* stream) {
+                                 int32_t n, int32_t rms_mode, int32_t* n_dropped, void* stream, int n_norm = 0,
+                                 const float* alpha_s = nullptr) {
   Geom g{};
   tpla_status st = make_geom(cfg, &g);
   if (st) return st;
@@ -517,9 +518,23 @@ static tpla_status append_common(const tpla_config* cfg, const tpla_weights* w, 
                 g.d_c / 32);
   cudaError_t e = launch_append_kv(g, w->xform_kind, static_cast<const float*>(w->xform), w->alpha_j, *cache,
                                    static_cast<const uint16_t*>(c_kv), static_cast<const uint16_t*>(k_pe), seq_idx,
-                                   pos, n, rms_mode, n_dropped, static_cast<cudaStream_t>(stream));
+                                   pos, n, rms_mode, n_dropped, static_cast<cudaStream_t>(stream), n_norm, alpha_s);
   if (e != cudaSuccess) return cuda_fail(e, "append_kv launch");
   return ok();
+}
+
+tpla_status tpla_append_kv_norm_only(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,
+                                     const void* c_kv, const void* k_pe, const int32_t* seq_idx, const int32_t* pos,
+                                     int32_t n, int32_t n_slices, const float* alpha, int32_t* n_dropped,
+                                     void* stream) {
+  if (!cfg || cfg->g != 1) return fail(TPLA_ERR_INVALID_ARG, "norm-only rows are g = 1 rows (the whole latent)");
+  if (n_slices < 1 || n_slices > 8 || (n_slices & (n_slices - 1)) || !alpha)
+    return fail(TPLA_ERR_INVALID_ARG, "n_slices=%d: a power of two in [1, 8], with alpha[n_slices]", n_slices);
+  for (int q = 0; q < n_slices; ++q)
+    if (!(alpha[q] > 0.f)) return fail(TPLA_ERR_INVALID_ARG, "alpha[%d] must be > 0", q);
+  if (cfg->d_c % (32 * n_slices) && !(w && w->xform_kind == TPLA_XFORM_PCA))
+    return fail(TPLA_ERR_UNSUPPORTED, "d_c=%d: slices must be whole lanes (d_c / 32 per lane)", cfg->d_c);
+  return append_common(cfg, w, cache, c_kv, k_pe, seq_idx, pos, n, TPLA_RMS_SLICED, n_dropped, stream, n_slices, alpha);
 }
 
 tpla_status tpla_append_kv(const tpla_config* cfg, const tpla_weights* w, const tpla_cache* cache,

@@ -148,6 +148,12 @@ class TplaRank:
         abi.tpla_append_kv(self.cfg, self.weights, self.cache, c_kv, k_pe, seq_idx, pos, n, rms_mode, n_dropped,
                            stream_ptr(stream))
 
+    def append_norm_only(self, c_kv, k_pe, seq_idx, pos, alpha, stream=None):
+        """g = 1 rows normalised per slice (SURVEY f4 "norm only"): len(alpha) slices."""
+        n = int(c_kv.shape[0])
+        abi.tpla_append_kv_norm_only(self.cfg, self.weights, self.cache, c_kv, k_pe, seq_idx, pos, n, alpha,
+                                     None, stream_ptr(stream))
+
     def prefill(self, c_kv, k_pe, seq_idx, pos, stream=None):
         n = int(c_kv.shape[0])
         abi.tpla_prefill_mla(self.cfg, self.weights, self.cache, c_kv, k_pe, seq_idx, pos, n, None,

@@ -879,3 +879,39 @@ def test_decode_v_two_stages_bit_identical():
             abi.tpla_decode_v(r.cfg, r.weights, r.cache, q, qpe, lens, B, 1, r.max_seq_len, r.ws, r.ws_bytes, v1, 1,
                               abi.DECODE_STAGE_PRE | abi.DECODE_STAGE_ATTN, 0)
         assert ei.value.status == abi.ERR_INVALID_ARG
+
+
+# ----------------------------------------------------------------------------- f4: "norm only" on the GPU
+@pytest.mark.parametrize("kind,n_slices", [("hadamard", 2), ("identity", 2), ("pca", 2), ("hadamard", 4),
+                                           ("pca", 8)])
+def test_norm_only_rows_equal_exact_logit_oracle(kind, n_slices):
+    """SURVEY f4 / Fig. 3 "TPLA (norm only)": sliced RMSNorm, one softmax over the summed partial
+    logits.  On the GPU: g = 1 rows normalised per slice (tpla_append_kv_norm_only) decoded by the g = 1
+    kernels (the CTA-pair K3) with mu = 1; oracle: tpla_decode_exact_logits over the k = g shards."""
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    S_list = [5, 130, 300]
+    B = len(S_list)
+    xf, sseed, U, U32, alpha = transform_inputs(kind, dims, 51, n_slices)
+    basis = U if kind == "pca" else None
+    w = synth.gen_weights(dims, 52)
+    q, qpe = synth.gen_queries(dims, B, 53)
+    c_raw = [synth.gen_raw_ckv(dims, S, 54, b, basis=basis) for b, S in enumerate(S_list)]
+    k_pe = [synth.gen_kpe(dims, S, 54, b) for b, S in enumerate(S_list)]
+    r = TplaRank(spec_of(dims), k=1, g=1, rank=0, batch=B, max_seq_len=max(S_list), device=d, page_perm_seed=3)
+    U_full = None if U32 is None else U32                    # PCA: all d_c columns at g = 1
+    r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=xf, sign_seed=sseed, U_pca=U_full, alpha=[1.0], mu=[1.0])
+    seq = np.concatenate([np.full(S, b, np.int32) for b, S in enumerate(S_list)])
+    pos = np.concatenate([np.arange(S, dtype=np.int32) for S in S_list])
+    r.append_norm_only(bf16_from_bits(np.concatenate(c_raw), d), bf16_from_bits(np.concatenate(k_pe), d),
+                       torch.from_numpy(seq).to(d), torch.from_numpy(pos).to(d), np.asarray(alpha, np.float32))
+    y = torch.zeros((B, dims.D), dtype=torch.float32, device=d)
+    r.decode(bf16_from_bits(q, d), bf16_from_bits(qpe, d), torch.tensor(S_list, dtype=torch.int32, device=d), y)
+    torch.cuda.synchronize()
+    pb = tpla.Problem(W_UK=f64(w.W_UK), W_UV=f64(w.W_UV), gamma=f64(w.gamma), W_O=f64(w.W_O), U=U,
+                      alpha=np.asarray(alpha, float), mu=np.ones(n_slices), c_raw=[f64(c) for c in c_raw],
+                      k_pe=[f64(x) for x in k_pe], modes=[[tpla.SLICED] * S for S in S_list], q_nope=f64(q),
+                      q_pe=f64(qpe), h_q=dims.h_q, d_h=dims.d_h, eps=1e-6, sm_scale=dims_scale(dims))
+    ref = tpla.tpla_decode_exact_logits(pb, n_slices, round_rows=numerics.round_bf16)   # (R19: the cache is bf16)
+    e = row_rel_err(y.cpu().numpy(), ref)
+    assert e <= TOL, e
