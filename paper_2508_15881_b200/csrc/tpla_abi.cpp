@@ -242,6 +242,7 @@ SplitPlan choose_split(int B, int max_seq_len) {
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+constexpr size_t kWsHeader = 64 << 10;   // decode workspace: [K3p plan | segment map] header, then Q'_j ...
 
 // The tcgen05 W^O GEMM takes at most kWoRows output rows per launch (the MMA N of its swap-AB
 // tile): larger batches run as consecutive row chunks sharing the partial workspace (each
@@ -274,15 +275,18 @@ WsLayout ws_layout(const Geom& g, int B, int n_q, int max_seq_len) {
   L.n_cta = tc_num_ctas(g, B, max_seq_len);
   const size_t parts = std::max(size_t(B) * sp.n_split, size_t(L.n_cta) + B);
   const size_t rows = size_t(n_q) * g.h_loc;            // partial rows per segment / split
-  size_t off = 0;
+  // the K3p plan and the segment map lead the workspace, in the same 2 MB page as Q'_j (the first
+  // global loads of every K3 CTA: plan, then Q'; one TLB walk instead of two)
+  L.plan = 0;
+  L.meta = align256(attn_plan_bytes(L.n_cta, B));
+  size_t off = std::max(kWsHeader, L.meta + align256(size_t(B) * 2 * 4));
   L.q_lat = off;   off += align256(size_t(R) * g.h_loc * g.w_lat * 2);
   L.o_part = off;  off += align256(parts * rows * g.w_lat * 4);
   L.ml_part = off; off += align256(parts * rows * 2 * 4);
   L.o_lat = off;   off += align256(size_t(R) * g.h_loc * g.w_lat * 2);
   L.v = off;       off += align256(size_t(R) * K * 2);
   L.y_part = off;  off += align256(size_t(L.kslices) * R * g.D * 4);
-  L.meta = off;    off += align256(size_t(B) * 2 * 4);
-  L.plan = off;    off += align256(attn_plan_bytes(L.n_cta, B));
+
   L.wo_part = off; off += align256(wo_tc_supported(g.D, K, std::min(R, kWoRows)) ? wo_tc_part_bytes(g.D, K, std::min(R, kWoRows)) : 0);
   L.total = off;
   return L;
@@ -845,8 +849,8 @@ static tpla_status project_out_common(const tpla_config* cfg, const tpla_weights
   if ((group_comm || comm) && !load_nccl()) return fail(TPLA_ERR_NCCL, "NCCL not loadable");
   const size_t v_bytes = align256(size_t(R) * kc * 2);
   const size_t part_bytes = wo_tc_part_bytes(g.D, kc, std::min(R, kWoRows));
-  if (ws_bytes < v_bytes + part_bytes)
-    return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, v_bytes + part_bytes);
+  if (ws_bytes < kWsHeader + v_bytes + part_bytes)
+    return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, kWsHeader + v_bytes + part_bytes);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const float* v_mine[kMaxSumSrc];
   for (int i = 0; i < n_v; ++i) v_mine[i] = v_list[i] + size_t(chunk) * R * kc;   // chunk c: [R, kc] contiguous
@@ -855,14 +859,14 @@ static tpla_status project_out_common(const tpla_config* cfg, const tpla_weights
                                           ncclSum, group_comm->comm, s);
     if (r != ncclSuccess) return fail(TPLA_ERR_NCCL, "ncclReduceScatter: %s", g_nccl.GetErrorString(r));
   }
-  auto* v16 = static_cast<uint16_t*>(ws);
+  auto* v16 = reinterpret_cast<uint16_t*>(static_cast<char*>(ws) + kWsHeader);   // (past the K3p plan)
   // v = bf16(Σ_j v_j), this slice (one source: the group sum is already in place)
   cudaError_t e = n_v == 1 ? launch_cast_bf16(v_mine[0], long(R) * kc, v16, s, "K5_v_cast")
                            : launch_sum_cast_bf16(v_mine, n_v, long(R) * kc, v16, s);
   if (e != cudaSuccess) return cuda_fail(e, "v cast");
   const FusedAr* ar = fused_ar(comm, R, g.D);                     // f2(i): the all-reduce in the K5 reduce
   uint16_t* out16 = (comm && !ar) ? nullptr : static_cast<uint16_t*>(out);
-  e = run_wo_tc(static_cast<const uint16_t*>(w->W_O), v16, g.D, K, R, static_cast<char*>(ws) + v_bytes, y,
+  e = run_wo_tc(static_cast<const uint16_t*>(w->W_O), v16, g.D, K, R, static_cast<char*>(ws) + kWsHeader + v_bytes, y,
                 (flags & TPLA_DECODE_ACCUMULATE) != 0, out16, s, chunk * kc, kc, ar);
   if (e != cudaSuccess) return cuda_fail(e, "K5b W_O (tcgen05)");
   if (comm && !ar) {                                               // C1: O = AllReduce(Σ Õ)
