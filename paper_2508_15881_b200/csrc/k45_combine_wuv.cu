@@ -16,6 +16,7 @@ namespace {
 constexpr int kMB = 16;     // batch rows per CTA (grid = heads x ceil(B/16))
 constexpr int kThreads = 32 * kMB;   // one warp per row: the merge is load-latency bound, so every
                                      // row's segment loads are in flight at once
+constexpr int kSegBatch = 4;        // segments (O row + (m, l)) in flight per lane
 
 struct FArgs {
   const float* o_part;      // [segs, H_loc, W_lat]
@@ -29,10 +30,9 @@ struct FArgs {
   int v_acc_add, v_chunks;  // column chunks [v_chunks][B * n_q][H_loc * d_h / v_chunks]
 };
 
-__global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
   pdl_trigger();
   extern __shared__ __align__(128) uint16_t smem[];
-  __shared__ float s_w[kMB][32];                    // per-row segment weights 2^(m_s - M)
   const int h = blockIdx.x;
   const int WP = a.w_lat + 8;                       // padded rows: conflict-free ldmatrix
   uint16_t* sW = smem;                              // [d_h][WP]
@@ -49,11 +49,14 @@ __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
   cp_async_commit();
   pdl_wait();
 
-  const int n_warps_n = a.d_h / 32;                 // warps along d_h (32 columns each)
   {
     const int m0 = blockIdx.y * kMB;
-    // ---- combine: warp w merges rows b = m0 + w, m0 + w + 8, ...
+    // ---- combine: warp w merges row m0 + w.  A row of W_lat fp32 is split over lpr lanes of 8 columns
+    // (two passes at W_lat = 512); the other 32 / lpr lane groups take every sp-th segment, in batches of
+    // kSegBatch independent loads (the merge is bound by load latency), summed across the groups at the end.
     const int n_rows = a.n_q * a.h_loc;             // partial rows per segment
+    const int lpr = a.w_lat / 8 < 32 ? a.w_lat / 8 : 32, sp = 32 / lpr;
+    const int sub = lane / lpr, cl = lane % lpr;
     for (int bi = warp; bi < kMB; bi += kThreads / 32) {
       const int bq = m0 + bi;                       // output row (sequence b, token i)
       const int b = bq / a.n_q, prow = (bq % a.n_q) * a.h_loc + h;
@@ -63,92 +66,109 @@ __global__ void __launch_bounds__(kThreads) combine_wuv_kernel(FArgs a) {
         continue;
       }
       const int s0 = a.meta[2 * b], s1 = a.meta[2 * b + 1];
-      float M = -INFINITY;
-      for (int s = s0 + lane; s <= s1; s += 32) M = fmaxf(M, a.ml_part[((long)s * n_rows + prow) * 2]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-      float L = 0.f;
-      for (int s = s0 + lane; s <= s1; s += 32) {
-        const float* ml = a.ml_part + ((long)s * n_rows + prow) * 2;
-        const float w = exp2f(ml[0] - M);
-        if (s - s0 < 32) s_w[warp][s - s0] = w;         // first 32 segment weights, for the merge
-        L += w * ml[1];
-      }
-      __syncwarp();
-      L = warp_sum(L);
-      const float inv = 1.f / L;
-      for (int c = lane * 8; c < a.w_lat; c += 256) {
+      // Online merge (running max, as in the attention itself): a segment's (m, l) and its O row are
+      // loaded together, so one batch of kSegBatch segments is one round trip.
+      const float2* mlp = reinterpret_cast<const float2*>(a.ml_part);
+      for (int c0 = 0; c0 < a.w_lat; c0 += lpr * 8) {
+        const int c = c0 + cl * 8;
+        float M = -INFINITY, L = 0.f;
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 8
-        for (int s = s0; s <= s1; ++s) {
-          // (lanes past W_lat have left this loop: no warp-collective ops in here)
-          const float wgt = s - s0 < 32 ? s_w[warp][s - s0] : exp2f(a.ml_part[((long)s * n_rows + prow) * 2] - M);
-          const float4* src = reinterpret_cast<const float4*>(a.o_part + ((long)s * n_rows + prow) * a.w_lat + c);
-          const float4 x0 = src[0], x1 = src[1];
-          acc[0] += wgt * x0.x; acc[1] += wgt * x0.y; acc[2] += wgt * x0.z; acc[3] += wgt * x0.w;
-          acc[4] += wgt * x1.x; acc[5] += wgt * x1.y; acc[6] += wgt * x1.z; acc[7] += wgt * x1.w;
+        for (int sb = s0 + sub; sb <= s1; sb += kSegBatch * sp) {
+          float4 x[kSegBatch][2];
+          float2 ml[kSegBatch];
+#pragma unroll
+          for (int i = 0; i < kSegBatch; ++i) {       // past s1: reload s1 (no divergent loads), weight 0
+            const int sg = sb + i * sp, sc = sg <= s1 ? sg : s1;
+            const float4* src = reinterpret_cast<const float4*>(a.o_part + ((long)sc * n_rows + prow) * a.w_lat + c);
+            x[i][0] = src[0];
+            x[i][1] = src[1];
+            ml[i] = mlp[(long)sc * n_rows + prow];
+          }
+          float Mn = M;
+#pragma unroll
+          for (int i = 0; i < kSegBatch; ++i)
+            if (sb + i * sp <= s1) Mn = fmaxf(Mn, ml[i].x);
+          const float r = exp2f(M - Mn);              // (M = -inf on the first batch: 0; Mn is finite)
+          L *= r;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] *= r;
+#pragma unroll
+          for (int i = 0; i < kSegBatch; ++i) {
+            const float w = sb + i * sp <= s1 ? exp2f(ml[i].x - Mn) : 0.f;
+            L += w * ml[i].y;
+            acc[0] += w * x[i][0].x; acc[1] += w * x[i][0].y; acc[2] += w * x[i][0].z; acc[3] += w * x[i][0].w;
+            acc[4] += w * x[i][1].x; acc[5] += w * x[i][1].y; acc[6] += w * x[i][1].z; acc[7] += w * x[i][1].w;
+          }
+          M = Mn;
         }
-        uint4 u;
-        u.x = pack_bf16(acc[0] * inv, acc[1] * inv);
-        u.y = pack_bf16(acc[2] * inv, acc[3] * inv);
-        u.z = pack_bf16(acc[4] * inv, acc[5] * inv);
-        u.w = pack_bf16(acc[6] * inv, acc[7] * inv);
-        *reinterpret_cast<uint4*>(arow + c) = u;
+        if (sp > 1) {                                 // merge the lane groups (segments sub, sub + sp, ...)
+          float Mg = M;
+#pragma unroll
+          for (int o = lpr; o < 32; o <<= 1) Mg = fmaxf(Mg, __shfl_xor_sync(0xffffffffu, Mg, o));
+          const float f = M == -INFINITY ? 0.f : exp2f(M - Mg);   // (a group without segments)
+          L *= f;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] *= f;
+#pragma unroll
+          for (int o = lpr; o < 32; o <<= 1) {
+            L += __shfl_xor_sync(0xffffffffu, L, o);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+          }
+        }
+        const float inv = 1.f / L;
+        if (sub == 0) {
+          uint4 u;
+          u.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+          u.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+          u.z = pack_bf16(acc[4] * inv, acc[5] * inv);
+          u.w = pack_bf16(acc[6] * inv, acc[7] * inv);
+          *reinterpret_cast<uint4*>(arow + c) = u;
+        }
       }
     }
     cp_async_wait<0>();
     __syncthreads();
-    // ---- v[m0.., h, :] = A [32 x W_lat] · W^UVᵀ: warp (mw, nw) owns rows 16*mw.. and columns 32*nw..
-    for (int task = warp; task < n_warps_n; task += kThreads / 32) {
-      const int mw = 0, nw = task;
-      float acc[4][4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    // ---- v[m0.., h, :] = A [16 x W_lat] · W^UVᵀ: warp w owns the 8 columns 8w.. (m16n8k16, full K)
+    for (int nw = warp; nw < a.d_h / 8; nw += kThreads / 32) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint16_t* brow = sW + (nw * 8 + (lane & 7)) * WP + (((lane >> 3) & 1) << 3);
+      const uint16_t* arow = sA + (lane & 15) * WP + ((lane >> 4) << 3);
+#pragma unroll 4
       for (int k0 = 0; k0 < a.w_lat; k0 += 16) {
-        uint32_t af[4];
-        ldmatrix_x4(af[0], af[1], af[2], af[3],
-                    smem_u32(sA + (mw * 16 + (lane & 15)) * WP + k0 + ((lane >> 4) << 3)));
-#pragma unroll
-        for (int nj = 0; nj < 2; ++nj) {
-          uint32_t b0, b1, b2, b3;
-          const int r = nw * 32 + nj * 16 + (lane & 7) + ((lane >> 4) << 3);
-          ldmatrix_x4(b0, b1, b2, b3, smem_u32(sW + r * WP + k0 + (((lane >> 3) & 1) << 3)));
-          uint32_t bb0[2] = {b0, b1}, bb1[2] = {b2, b3};
-          mma_bf16_16816(acc[2 * nj], af, bb0);
-          mma_bf16_16816(acc[2 * nj + 1], af, bb1);
-        }
+        uint32_t af[4], bf[2];
+        ldmatrix_x4(af[0], af[1], af[2], af[3], smem_u32(arow + k0));
+        ldmatrix_x2(bf[0], bf[1], smem_u32(brow + k0));
+        mma_bf16_16816(acc, af, bf);
       }
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int b = m0 + mw * 16 + (lane >> 2) + hh * 8;
-          const int e = nw * 32 + ni * 8 + (lane & 3) * 2;
-          if (b < a.B * a.n_q) {
-            if (a.v_acc) {                          // (each element has exactly one writer: no atomics)
-              const int kc = a.h_loc * a.d_h / a.v_chunks, c = h * a.d_h + e;   // (kc even: e, c even)
-              const long idx = (long(c / kc) * a.B * a.n_q + b) * kc + c % kc;
-              float2 o = make_float2(acc[ni][2 * hh], acc[ni][2 * hh + 1]);
-              if (a.v_acc_add) {
-                const float2 p = *reinterpret_cast<const float2*>(a.v_acc + idx);
-                o.x += p.x;
-                o.y += p.y;
-              }
-              *reinterpret_cast<float2*>(a.v_acc + idx) = o;
-            } else {
-              const long idx = (long)b * a.h_loc * a.d_h + h * a.d_h + e;
-              *reinterpret_cast<uint32_t*>(a.v + idx) = pack_bf16(acc[ni][2 * hh], acc[ni][2 * hh + 1]);
+      for (int hh = 0; hh < 2; ++hh) {
+        const int b = m0 + (lane >> 2) + hh * 8;
+        const int e = nw * 8 + (lane & 3) * 2;
+        if (b < a.B * a.n_q) {
+          if (a.v_acc) {                            // (each element has exactly one writer: no atomics)
+            const int kc = a.h_loc * a.d_h / a.v_chunks, c = h * a.d_h + e;   // (kc even: e, c even)
+            const long idx = (long(c / kc) * a.B * a.n_q + b) * kc + c % kc;
+            float2 o = make_float2(acc[2 * hh], acc[2 * hh + 1]);
+            if (a.v_acc_add) {
+              const float2 p = *reinterpret_cast<const float2*>(a.v_acc + idx);
+              o.x += p.x;
+              o.y += p.y;
             }
+            *reinterpret_cast<float2*>(a.v_acc + idx) = o;
+          } else {
+            const long idx = (long)b * a.h_loc * a.d_h + h * a.d_h + e;
+            *reinterpret_cast<uint32_t*>(a.v + idx) = pack_bf16(acc[2 * hh], acc[2 * hh + 1]);
           }
         }
+      }
     }
-    __syncthreads();
   }
 }
 
 }  // namespace
 
-bool combine_wuv_supported(const Geom& g) { return g.d_h % 32 == 0 && g.w_lat % 64 == 0 && g.w_lat <= 512; }
+bool combine_wuv_supported(const Geom& g) { return g.d_h % 8 == 0 && g.w_lat % 64 == 0 && g.w_lat <= 512; }
 
 cudaError_t launch_combine_wuv(const Geom& g, int B, int n_q, const float* o_part, const float* ml_part,
                                const int32_t* meta, const uint16_t* W_UV, uint16_t* v, cudaStream_t s,
