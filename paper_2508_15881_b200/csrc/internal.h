@@ -89,6 +89,12 @@ int tc_num_ctas(const Geom& g, int B, int max_seq_len);
 size_t attn_plan_bytes(int n_cta, int B);
 cudaError_t launch_attn_plan(const Geom& g, const tpla_cache& cache, const int32_t* seq_lens, int B, int n_cta,
                              int32_t* plan, cudaStream_t s);
+// K3p + K2 fused (one launch): the schedule as launch_attn_plan, and Q'_j = W^UK'_j q (TMA-staged
+// per (head, 32 rows)); q_nope [R, h_q*d_h] all heads, W_UK [H_loc, W_lat, d_h], q_lat [R, H_loc, W_lat]
+bool pre_attn_supported(const Geom& g);
+cudaError_t launch_pre_attn(const Geom& g, const tpla_cache& cache, const int32_t* seq_lens, int B, int n_cta,
+                            int32_t* plan, const uint16_t* W_UK, const uint16_t* q_nope, int R, uint16_t* q_lat,
+                            cudaStream_t s);
 cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
                                   const int32_t* seq_lens, int B, int n_q, int n_cta, const int32_t* plan,
                                   float* o_part, float* ml_part, int32_t* meta, cudaStream_t s);

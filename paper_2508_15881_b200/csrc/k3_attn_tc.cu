@@ -239,8 +239,7 @@ constexpr int kPlanThreads = 512;
 constexpr int kPlanRowCtas = kPlanThreads / 32;           // K3 CTAs whose rows one plan CTA resolves
 
 template <int W_LAT>
-__global__ void __launch_bounds__(kPlanThreads) attn_plan_kernel(PlanArgs p) {
-  pdl_trigger();
+__device__ __forceinline__ void plan_body(const PlanArgs& p, int cta) {   // cta: this CTA's index in K3p's grid
   using C = Cfg<W_LAT>;
   __shared__ int cum[kMaxB + 1], slen[kMaxB], lo_arr[kMaxCta + 1], wsum[40];
   const int tid = threadIdx.x;
@@ -253,7 +252,7 @@ __global__ void __launch_bounds__(kPlanThreads) attn_plan_kernel(PlanArgs p) {
   __syncthreads();
   const int n = p.n_cta;
   const long Wt = long(total) + long(C::SEQ_COST) * p.B;            // total work units
-  if (blockIdx.x == 0) {
+  if (cta == 0) {
     for (int cc = tid; cc <= n; cc += kPlanThreads) lo_arr[cc] = tile_of<C::SEQ_COST>(cum, p.B, cc * Wt / n);
     __syncthreads();
     int lo = 0, hi = 0, bf = 0, bl = -1;
@@ -278,7 +277,7 @@ __global__ void __launch_bounds__(kPlanThreads) attn_plan_kernel(PlanArgs p) {
     return;
   }
   // first 32 box rows of K3 CTAs [c0, c0 + kPlanRowCtas)
-  const int c0 = (blockIdx.x - 1) * kPlanRowCtas, cc = c0 + tid / 32, u = tid & 31;
+  const int c0 = (cta - 1) * kPlanRowCtas, cc = c0 + tid / 32, u = tid & 31;
   int row = 0;
   if (cc < n) {
     const int lo = tile_of<C::SEQ_COST>(cum, p.B, cc * Wt / n), hi = tile_of<C::SEQ_COST>(cum, p.B, (cc + 1) * Wt / n);
@@ -293,6 +292,33 @@ __global__ void __launch_bounds__(kPlanThreads) attn_plan_kernel(PlanArgs p) {
   }
   pdl_wait();
   if (cc < n) p.plan[n * kPlanStride + 2 * p.B + 1 + cc * 32 + u] = row;
+}
+
+template <int W_LAT>
+__global__ void __launch_bounds__(kPlanThreads) attn_plan_kernel(PlanArgs p) {
+  pdl_trigger();
+  plan_body<W_LAT>(p, blockIdx.x);
+}
+
+inline int plan_ctas(int n_cta) { return 1 + (n_cta + kPlanRowCtas - 1) / kPlanRowCtas; }
+
+#include "k2_absorb.cuh"
+
+// K3p + K2 in one launch (the two are independent: K3p reads seq_lens / the block table, K2 the
+// queries and W^UK'): the first plan_ctas(n_cta) CTAs compute K3's schedule, the others one
+// (head, 32-row tile) of Q'_j each.  One launch and one PDL hop fewer ahead of K3.
+template <int W_LAT>
+__global__ void __launch_bounds__(kPlanThreads) pre_attn_kernel(const __grid_constant__ CUtensorMap wmap,
+                                                                const __grid_constant__ CUtensorMap qmap, PlanArgs p,
+                                                                absorb::Args a, int n_plan) {
+  pdl_trigger();
+  if (int(blockIdx.x) < n_plan) {
+    plan_body<W_LAT>(p, blockIdx.x);
+    return;
+  }
+  extern __shared__ __align__(1024) uint8_t pre_smem[];
+  __shared__ uint64_t bar;
+  absorb::body(&wmap, &qmap, a, blockIdx.x - n_plan, pre_smem, &bar);
 }
 
 // MODE 0: the kernel.  MODE 1 (diagnostic, TPLA_K3_MODE=stream): the TMA ring alone — every
@@ -1208,12 +1234,16 @@ bool tc_attention_supported(const Geom& g, int B) {
 // At least kMinBoxes 64-token boxes per CTA: with one box each (small batch x short context) a
 // CTA's fixed costs dominate — its epilogue writes a 128 x W_lat fp32 partial (3x the bytes of a
 // 64-token C1 tile) and the merge then reads one partial per CTA (measured at batch 1, 4K: K3
-// 19 us and K45 26 us per rank with 64 one-box CTAs).
-constexpr long kMinBoxes = 4;
+// 19 us and K45 26 us per rank with 64 one-box CTAs).  8 boxes (512 tokens) per CTA, measured over
+// context 4K-64K x batch 1-8 (tools/gpu_minboxes.sh): per rank, K3 + K45 within 1 us of the 4-box floor,
+// half the partials; with the two co-located ranks of the bench the K3s then share the SMs (32K
+// batch 1: step 101 -> 84 us).  Large batches are unaffected (the grid is the SM count there).
+constexpr long kMinBoxes = 8;
 int tc_num_ctas(const Geom& g, int B, int max_seq_len) {
   long boxes = (long)B * ((max_seq_len + kSub - 1) / kSub);
   const int slots = g.w_lat == 512 ? num_sms() / 2 : num_sms();   // W_lat = 512: CTA pairs
-  return int(std::max(1L, std::min<long>(std::min(slots, kMaxCta), boxes / kMinBoxes)));
+  static const long min_boxes = getenv("TPLA_K3_MIN_BOXES") ? std::max(1L, atol(getenv("TPLA_K3_MIN_BOXES"))) : kMinBoxes;
+  return int(std::max(1L, std::min<long>(std::min(slots, kMaxCta), boxes / min_boxes)));
 }
 
 size_t attn_plan_bytes(int n_cta, int B) {
@@ -1223,7 +1253,23 @@ size_t attn_plan_bytes(int n_cta, int B) {
 template <int W_LAT>
 cudaError_t launch_plan_w(const PlanArgs& p, cudaStream_t s) {
   KernelScope ks("K3p_attn_plan", s);
-  return launch_k(attn_plan_kernel<W_LAT>, 1 + (p.n_cta + kPlanRowCtas - 1) / kPlanRowCtas, kPlanThreads, 0, s, p);
+  return launch_k(attn_plan_kernel<W_LAT>, plan_ctas(p.n_cta), kPlanThreads, 0, s, p);
+}
+
+template <int W_LAT>
+cudaError_t launch_pre_w(const CUtensorMap& wmap, const CUtensorMap& qmap, const PlanArgs& p, const absorb::Args& a,
+                         cudaStream_t s) {
+  const size_t smem = absorb::smem_bytes(a.w_lat, a.d_h);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(pre_attn_kernel<W_LAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  const int n_plan = plan_ctas(p.n_cta);
+  const int n_items = a.h_loc * ((a.R + absorb::kRows - 1) / absorb::kRows);
+  KernelScope ks("K3p_K2_pre_attn", s);
+  return launch_k(pre_attn_kernel<W_LAT>, n_plan + n_items, kPlanThreads, smem, s, wmap, qmap, p, a, n_plan);
 }
 
 cudaError_t launch_attn_plan(const Geom& g, const tpla_cache& cache, const int32_t* seq_lens, int B, int n_cta,
@@ -1236,6 +1282,39 @@ cudaError_t launch_attn_plan(const Geom& g, const tpla_cache& cache, const int32
     case 128: return launch_plan_w<128>(p, s);
     case 256: return launch_plan_w<256>(p, s);
     case 512: return launch_plan_w<512>(p, s);
+  }
+  return cudaErrorNotSupported;
+}
+
+bool pre_attn_supported(const Geom& g) { return absorb::supported(g.w_lat, g.d_h); }
+
+cudaError_t launch_pre_attn(const Geom& g, const tpla_cache& cache, const int32_t* seq_lens, int B, int n_cta,
+                            int32_t* plan, const uint16_t* W_UK, const uint16_t* q_nope, int R, uint16_t* q_lat,
+                            cudaStream_t s) {
+  if (B > kMaxB || n_cta > kMaxCta || !pre_attn_supported(g)) return cudaErrorInvalidValue;
+  EncodeFn enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  auto map2d = [&](CUtensorMap* m, const void* base, long cols, long rows, int box_c, int box_r) {
+    cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
+    cuuint32_t box[2] = {cuuint32_t(box_c), cuuint32_t(box_r)};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  CUtensorMap wmap, qmap;
+  if (!map2d(&wmap, W_UK, g.d_h, long(g.h_loc) * g.w_lat, 64, std::min(g.w_lat, 256)) ||
+      !map2d(&qmap, q_nope, long(g.h_q) * g.d_h, R, 64, absorb::kRows))
+    return cudaErrorInvalidValue;
+  PlanArgs p{seq_lens, cache.block_table, plan, B, n_cta, cache.max_pages_per_seq * cache.page_size, cache.page_size,
+             cache.max_pages_per_seq};
+  absorb::Args a{q_lat, R, g.h_loc, g.w_lat, g.d_h, g.head_begin * g.d_h};
+  switch (g.w_lat) {
+    case 64: return launch_pre_w<64>(wmap, qmap, p, a, s);
+    case 128: return launch_pre_w<128>(wmap, qmap, p, a, s);
+    case 256: return launch_pre_w<256>(wmap, qmap, p, a, s);
+    case 512: return launch_pre_w<512>(wmap, qmap, p, a, s);
   }
   return cudaErrorNotSupported;
 }

@@ -33,6 +33,7 @@ struct FArgs {
 __global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
   pdl_trigger();
   extern __shared__ __align__(128) uint16_t smem[];
+  __shared__ float s_ml[kMB][2];                   // per-warp (M, L) of a split row (wpr > 1)
   const int h = blockIdx.x;
   const int WP = a.w_lat + 8;                       // padded rows: conflict-free ldmatrix
   uint16_t* sW = smem;                              // [d_h][WP]
@@ -51,20 +52,26 @@ __global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
 
   {
     const int m0 = blockIdx.y * kMB;
-    // ---- combine: warp w merges row m0 + w.  A row of W_lat fp32 is split over lpr lanes of 8 columns
-    // (two passes at W_lat = 512); the other 32 / lpr lane groups take every sp-th segment, in batches of
-    // kSegBatch independent loads (the merge is bound by load latency), summed across the groups at the end.
+    // ---- combine.  The CTA's R_c rows share the 16 warps: wpr = 16 / pow2ceil(R_c) warps per row (one
+    // at B >= 16; all 16 for a single sequence, whose K3 segments number up to the grid size).  A row of
+    // W_lat fp32 is split over lpr lanes of 8 columns (two passes at W_lat = 512); the 32 / lpr lane
+    // groups of each of the row's wpr warps take every NG-th segment, NG = wpr * 32 / lpr, in batches of
+    // kSegBatch independent loads (the merge is bound by load latency).  Groups merge by shuffles in a
+    // warp, then (wpr > 1) through shared memory.
     const int n_rows = a.n_q * a.h_loc;             // partial rows per segment
     const int lpr = a.w_lat / 8 < 32 ? a.w_lat / 8 : 32, sp = 32 / lpr;
     const int sub = lane / lpr, cl = lane % lpr;
-    for (int bi = warp; bi < kMB; bi += kThreads / 32) {
+    const int R_c = min(kMB, a.B * a.n_q - m0);
+    int rp = 1;
+    while (rp < R_c) rp <<= 1;
+    const int wpr = kMB / rp, bi = warp / wpr, part = warp % wpr, NG = wpr * sp, G = part * sp + sub;
+    float* scr = reinterpret_cast<float*>(sA + kMB * WP);   // [16 warps][W_lat] fp32 (wpr > 1)
+    for (int r = R_c + warp; r < kMB; r += kThreads / 32)    // rows past B * n_q: zero A rows
+      for (int c = lane * 8; c < a.w_lat; c += 256) *reinterpret_cast<uint4*>(sA + r * WP + c) = make_uint4(0, 0, 0, 0);
+    if (bi < R_c) {
       const int bq = m0 + bi;                       // output row (sequence b, token i)
       const int b = bq / a.n_q, prow = (bq % a.n_q) * a.h_loc + h;
       uint16_t* arow = sA + bi * WP;
-      if (bq >= a.B * a.n_q) {
-        for (int c = lane * 8; c < a.w_lat; c += 256) *reinterpret_cast<uint4*>(arow + c) = make_uint4(0, 0, 0, 0);
-        continue;
-      }
       const int s0 = a.meta[2 * b], s1 = a.meta[2 * b + 1];
       // Online merge (running max, as in the attention itself): a segment's (m, l) and its O row are
       // loaded together, so one batch of kSegBatch segments is one round trip.
@@ -73,12 +80,12 @@ __global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
         const int c = c0 + cl * 8;
         float M = -INFINITY, L = 0.f;
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int sb = s0 + sub; sb <= s1; sb += kSegBatch * sp) {
+        for (int sb = s0 + G; sb <= s1; sb += kSegBatch * NG) {
           float4 x[kSegBatch][2];
           float2 ml[kSegBatch];
 #pragma unroll
           for (int i = 0; i < kSegBatch; ++i) {       // past s1: reload s1 (no divergent loads), weight 0
-            const int sg = sb + i * sp, sc = sg <= s1 ? sg : s1;
+            const int sg = sb + i * NG, sc = sg <= s1 ? sg : s1;
             const float4* src = reinterpret_cast<const float4*>(a.o_part + ((long)sc * n_rows + prow) * a.w_lat + c);
             x[i][0] = src[0];
             x[i][1] = src[1];
@@ -87,21 +94,21 @@ __global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
           float Mn = M;
 #pragma unroll
           for (int i = 0; i < kSegBatch; ++i)
-            if (sb + i * sp <= s1) Mn = fmaxf(Mn, ml[i].x);
+            if (sb + i * NG <= s1) Mn = fmaxf(Mn, ml[i].x);
           const float r = exp2f(M - Mn);              // (M = -inf on the first batch: 0; Mn is finite)
           L *= r;
 #pragma unroll
           for (int e = 0; e < 8; ++e) acc[e] *= r;
 #pragma unroll
           for (int i = 0; i < kSegBatch; ++i) {
-            const float w = sb + i * sp <= s1 ? exp2f(ml[i].x - Mn) : 0.f;
+            const float w = sb + i * NG <= s1 ? exp2f(ml[i].x - Mn) : 0.f;
             L += w * ml[i].y;
             acc[0] += w * x[i][0].x; acc[1] += w * x[i][0].y; acc[2] += w * x[i][0].z; acc[3] += w * x[i][0].w;
             acc[4] += w * x[i][1].x; acc[5] += w * x[i][1].y; acc[6] += w * x[i][1].z; acc[7] += w * x[i][1].w;
           }
           M = Mn;
         }
-        if (sp > 1) {                                 // merge the lane groups (segments sub, sub + sp, ...)
+        if (sp > 1) {                                 // merge the lane groups of this warp
           float Mg = M;
 #pragma unroll
           for (int o = lpr; o < 32; o <<= 1) Mg = fmaxf(Mg, __shfl_xor_sync(0xffffffffu, Mg, o));
@@ -115,6 +122,16 @@ __global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
           }
+          M = Mg;
+        }
+        if (wpr > 1) {                                // this warp's share, unnormalised, for the row's merge
+          if (sub == 0) {
+            float4* d = reinterpret_cast<float4*>(scr + warp * a.w_lat + c);
+            d[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            d[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+          }
+          if (lane == 0) { s_ml[warp][0] = M; s_ml[warp][1] = L; }
+          continue;
         }
         const float inv = 1.f / L;
         if (sub == 0) {
@@ -124,6 +141,39 @@ __global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
           u.z = pack_bf16(acc[4] * inv, acc[5] * inv);
           u.w = pack_bf16(acc[6] * inv, acc[7] * inv);
           *reinterpret_cast<uint4*>(arow + c) = u;
+        }
+      }
+    }
+    if (wpr > 1) {                                    // (CTA-uniform) merge the row's wpr warps, in warp order
+      __syncthreads();
+      if (bi < R_c && part == 0) {
+        float Mg = -INFINITY;
+        for (int p = 0; p < wpr; ++p) Mg = fmaxf(Mg, s_ml[warp + p][0]);
+        // lane p < wpr: warp p's weight 2^(M_p - M), broadcast by shuffles below
+        const float Mp = lane < wpr ? s_ml[warp + lane][0] : -INFINITY;
+        const float fl = Mp == -INFINITY ? 0.f : exp2f(Mp - Mg);
+        const float L = warp_sum(lane < wpr ? fl * s_ml[warp + lane][1] : 0.f);
+        const float inv = 1.f / L;
+        float4 o[4];                                  // columns lane * 4 + 128 j (W_lat <= 512)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int p = 0; p < wpr; ++p) {
+          const float fp = __shfl_sync(0xffffffffu, fl, p);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int c = lane * 4 + 128 * j;
+            if (c < a.w_lat) {
+              const float4 x = *reinterpret_cast<const float4*>(scr + (warp + p) * a.w_lat + c);
+              o[j].x += fp * x.x; o[j].y += fp * x.y; o[j].z += fp * x.z; o[j].w += fp * x.w;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = lane * 4 + 128 * j;
+          if (c < a.w_lat)
+            *reinterpret_cast<uint2*>(sA + bi * WP + c) = make_uint2(pack_bf16(o[j].x * inv, o[j].y * inv),
+                                                                     pack_bf16(o[j].z * inv, o[j].w * inv));
         }
       }
     }
@@ -174,7 +224,7 @@ cudaError_t launch_combine_wuv(const Geom& g, int B, int n_q, const float* o_par
                                const int32_t* meta, const uint16_t* W_UV, uint16_t* v, cudaStream_t s,
                                float* v_acc, bool v_acc_add, int v_chunks) {
   FArgs a{o_part, ml_part, meta, W_UV, v, B, g.h_loc, g.w_lat, g.d_h, n_q, v_acc, v_acc_add ? 1 : 0, v_chunks};
-  const size_t smem = size_t(g.d_h + kMB) * (g.w_lat + 8) * 2;
+  const size_t smem = size_t(g.d_h + kMB) * (g.w_lat + 8) * 2 + size_t(kMB) * g.w_lat * 4;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(combine_wuv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

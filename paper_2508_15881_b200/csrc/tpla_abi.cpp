@@ -248,6 +248,20 @@ constexpr size_t kWsHeader = 64 << 10;   // decode workspace: [K3p plan | segmen
 // tile): larger batches run as consecutive row chunks sharing the partial workspace (each
 // chunk's GEMM waits for the previous chunk's reduce before writing it: PDL wait at entry).
 constexpr int kWoRows = 256;
+// K3p (when the persistent K3 follows) and K2 ahead of the attention: one fused launch where the
+// shapes allow (TPLA_PRE_SPLIT=1: the two separate kernels, for A/B), else K3p then the mma.sync K2.
+static cudaError_t launch_pre(const Geom& g, const tpla_cache& cache, const int32_t* seq_lens, int B, int n_cta,
+                              int32_t* plan, bool with_plan, const uint16_t* W_UK, const uint16_t* qn, int R,
+                              uint16_t* q_lat, cudaStream_t s) {
+  static const bool split = getenv("TPLA_PRE_SPLIT") && atoi(getenv("TPLA_PRE_SPLIT")) != 0;
+  if (with_plan && !split && pre_attn_supported(g))
+    return launch_pre_attn(g, cache, seq_lens, B, n_cta, plan, W_UK, qn, R, q_lat, s);
+  cudaError_t e = cudaSuccess;
+  if (with_plan && (e = launch_attn_plan(g, cache, seq_lens, B, n_cta, plan, s)) != cudaSuccess) return e;
+  return launch_head_gemv("K2_absorb_q", W_UK, qn + size_t(g.head_begin) * g.d_h, long(g.h_q) * g.d_h, g.h_loc,
+                          g.w_lat, g.d_h, R, q_lat, true, s);
+}
+
 static cudaError_t run_wo_tc(const uint16_t* Wo, const uint16_t* v, int D, int K, int R, void* part, float* y,
                              bool accumulate, uint16_t* out16, cudaStream_t s, int k_begin = 0, int k_len = 0,
                              const FusedAr* ar = nullptr) {
@@ -626,14 +640,9 @@ tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const
   cudaError_t e;
   const bool tc_path = use_tc_attention(g, B) && combine_wuv_supported(g);
   auto* plan = reinterpret_cast<int32_t*>(base + L.plan);
-  if (tc_path) {   // K3p: K3's schedule, ahead of K2 (its latency hides under K1 / K2)
-    e = launch_attn_plan(g, *cache, seq_lens, B, L.n_cta, plan, s);
-    if (e != cudaSuccess) return cuda_fail(e, "K3p plan");
-  }
-  // K2: Q'_j[b,h,:] = W^UK'_j[h] q[b,h,:]   (mu_j folded)
-  e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK), qn + size_t(g.head_begin) * g.d_h,
-                       long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h, R, q_lat, true, s);
-  if (e != cudaSuccess) return cuda_fail(e, "K2 absorb_q");
+  // K3p (K3's schedule) and K2: Q'_j[b,h,:] = W^UK'_j[h] q[b,h,:]   (mu_j folded)
+  e = launch_pre(g, *cache, seq_lens, B, L.n_cta, plan, tc_path, static_cast<const uint16_t*>(w->W_UK), qn, R, q_lat, s);
+  if (e != cudaSuccess) return cuda_fail(e, "K3p/K2 pre-attention");
   if (tc_path) {
     // K3: per-shard split-K flash decoding (Eq. tpla_softmax_one_device) -> partials;
     // K4 + K5a fused: merge the partials of each (b, h) into O_j and apply W^UV'_j
@@ -804,11 +813,9 @@ tpla_status tpla_decode_v(const tpla_config* cfg, const tpla_weights* w, const t
   if (!pre && !attn) return fail(TPLA_ERR_INVALID_ARG, "STAGE_PRE and STAGE_ATTN together");
   cudaError_t e = cudaSuccess;
   if (pre) {
-    e = launch_attn_plan(g, *cache, seq_lens, B, L.n_cta, plan, s);   // K3p, ahead of K2
-    if (e != cudaSuccess) return cuda_fail(e, "K3p plan");
-    e = launch_head_gemv("K2_absorb_q", static_cast<const uint16_t*>(w->W_UK), qn + size_t(g.head_begin) * g.d_h,
-                         long(g.h_q) * g.d_h, g.h_loc, g.w_lat, g.d_h, B * n_q, q_lat, true, s);
-    if (e != cudaSuccess) return cuda_fail(e, "K2 absorb_q");
+    e = launch_pre(g, *cache, seq_lens, B, L.n_cta, plan, true, static_cast<const uint16_t*>(w->W_UK), qn, B * n_q,
+                   q_lat, s);
+    if (e != cudaSuccess) return cuda_fail(e, "K3p/K2 pre-attention");
   }
   if (!attn) return ok();
   e = launch_decode_attn_tc(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, n_q, L.n_cta, plan,

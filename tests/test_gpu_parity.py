@@ -621,6 +621,14 @@ def test_e2e_parity_ragged_combine_blocks():
 
 
 # ----------------------------------------------------------------------------- round-2 parity cases
+@pytest.mark.parametrize("k,g,S_list", [(2, 2, [12000]), (8, 8, [5000, 700, 9000]), (2, 2, [3000, 6000])])
+def test_e2e_parity_small_batch_many_segments(k, g, S_list):
+    """Small batch x long context: K3 splits each sequence over tens of CTAs (segments), and K45's
+    16 warps share a CTA's few rows (16 / pow2ceil(rows) warps per row, merged through shared memory)."""
+    e2e_case(dev(), synth.PRESETS["dsv3"], k, g, "hadamard", S_list)
+    e2e_case(dev(), synth.PRESETS["dsv3"], k, g, "hadamard", S_list, wo="shared")
+
+
 @pytest.mark.parametrize("dname,k,g,kind", [("dsv3", 2, 2, "hadamard"), ("dsv3", 8, 8, "hadamard"),
                                             ("kimi", 4, 4, "identity"), ("tiny", 2, 2, "pca")])
 def test_e2e_parity_mu_one(dname, k, g, kind):
