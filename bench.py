@@ -74,6 +74,7 @@ def parse():
     p.add_argument("--workload", default="c1", choices=sorted(WORKLOADS))
     p.add_argument("--impl", default="tpla", choices=["tpla", "reference"])
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-diag", action="store_true", help="stderr: per-step graph replay timings behind e2e")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-headline", action="store_true", help="skip the h8 K3 headline record")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the cpu_baseline sample")
@@ -700,7 +701,7 @@ def main():
         d_out = [torch.empty_like(out) for _ in range(2)]
         h2d = sum(t.numel() * t.element_size() for t in (h_ck[0], h_kp[0], h_q[0], h_qp[0]))
         d2h = h_out[0].numel() * h_out[0].element_size()
-        n_e2e = max(10, min(args.steps, 100))
+        n_e2e = min(max(args.steps, 100), 200)           # (>= 100 steps: host jitter amortised)
         for i in range(3):
             step(i, *d_in[i & 1], o=d_out[i & 1])
         g1 = [None, None]
@@ -747,6 +748,39 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1))
+        if args.e2e_diag and g1[0] is not None:
+            # where the e2e time goes: per-step graph replays back to back (no copies, no host waits),
+            # then with the cross-stream event waits, then with the host waiting for every output
+            def timed(fn):
+                torch.cuda.synchronize()
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                fn()
+                a1.record(stream)
+                torch.cuda.synchronize()
+                return a0.elapsed_time(a1) / n_e2e * 1e3
+            def replays():
+                for i in range(n_e2e):
+                    g1[i & 1].replay()
+            def replays_ev():
+                for i in range(n_e2e):
+                    s = i & 1
+                    with torch.cuda.stream(cs_in):
+                        ev_in[s].record(cs_in)
+                    stream.wait_event(ev_in[s])
+                    g1[s].replay()
+                    ev_done[s].record(stream)
+            def replays_sync():
+                for i in range(n_e2e):
+                    s = i & 1
+                    g1[s].replay()
+                    ev_done[s].record(stream)
+                    if i >= 1:
+                        ev_done[s ^ 1].synchronize()
+            print(json.dumps({"e2e_diag_us_per_step": {"graph_per_step": timed(replays),
+                                                       "with_event_waits": timed(replays_ev),
+                                                       "with_host_wait": timed(replays_sync),
+                                                       "e2e": ems / n_e2e * 1e3}}), file=sys.stderr)
         e2e = {"value": B * nq * n_e2e / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": n_e2e, "ms_per_step": ems / n_e2e,
                "pipeline": "double-buffered: H2D of step i and D2H of step i-1 on copy streams, "
