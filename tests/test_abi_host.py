@@ -220,3 +220,30 @@ def test_decode_kernel_path_reported():
     with pytest.raises(abi.TplaError) as ei:
         abi.tpla_decode_kernel_path(cfg(g=3, k=3), 1)
     assert ei.value.status == abi.ERR_DIVISIBILITY
+
+
+def build_c_example(out_dir):
+    """gcc -std=c99 of examples/decode_step.c against include/tpla.h and libtpla.so: the boundary
+    is usable from plain C (no Python, no C++)."""
+    lib_dir = os.path.dirname(abi.LIB_PATH)
+    exe = os.path.join(str(out_dir), "decode_step")
+    cmd = ["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-O1", "-I" + os.path.join(ROOT, "include"),
+           "-I/usr/local/cuda/include", os.path.join(ROOT, "examples", "decode_step.c"), "-o", exe,
+           "-L" + lib_dir, "-ltpla", "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath," + lib_dir,
+           "-Wl,-rpath,/usr/local/cuda/lib64", "-lm"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_example_builds(tmp_path):
+    exe = build_c_example(tmp_path)
+    out = subprocess.run(["nm", "-u", exe], capture_output=True, text=True).stdout
+    assert "tpla_decode" in out and "tpla_convert_weights" in out      # resolved from libtpla.so
+
+
+def test_header_is_c99():
+    src = '#include "tpla.h"\nint main(void) { tpla_config c; (void)c; return TPLA_OK; }\n'
+    r = subprocess.run(["gcc", "-std=c99", "-pedantic", "-Wall", "-Wextra", "-Werror", "-I" + os.path.join(ROOT, "include"),
+                        "-x", "c", "-fsyntax-only", "-"], input=src, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

@@ -946,3 +946,14 @@ def test_prefill_mla_forward_graph_replay_deterministic():
     graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(yg, y0) and torch.isfinite(y0).all()
+
+
+def test_c_example_runs_on_gpu(tmp_path):
+    """examples/decode_step.c: convert, append and a two-rank decode step through the C ABI alone
+    (tcgen05 path), finite and bit-identical on replay, bad batch rejected before any launch."""
+    import subprocess
+    from test_abi_host import build_c_example
+    exe = build_c_example(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "decode_step OK" in r.stdout and "K3 path: 1" in r.stdout, r.stdout
