@@ -87,8 +87,13 @@ def parse():
                    help="up-projection: 'rank' = every rank multiplies its own v_j by its W^O rows (P:139-141); "
                         "'shared' = the g ranks of a head block sum v first and read W^O once, reduce-scattered "
                         "across processes (SURVEY f2(ii)); auto = shared when g > 1")
-    p.add_argument("--no-fused-ar", action="store_true",
-                   help="N > 1: plain ncclAllReduce after the W^O GEMM instead of the fused one-shot all-reduce")
+    p.add_argument("--fused-ar", action="store_true",
+                   help="N > 1: the fused one-shot all-reduce in the W^O epilogue (SURVEY f2(i); validated at world "
+                        "1 only) instead of the plain ncclAllReduce")
+    p.add_argument("--no-fused-ar", action="store_true", help="(default; kept for compatibility)")
+    p.add_argument("--watchdog", type=float, default=1200.0,
+                   help="N > 1: seconds after which a run that has not finished prints why and exits 3 "
+                        "(a collective that never completes would otherwise hang the launcher)")
     p.add_argument("--rank-streams", default="auto", choices=["auto", "off", "full", "pre"],
                    help="co-located ranks of a latent group: off = serially on one stream; full = one stream per rank "
                         "(separate v accumulators summed in tpla_project_out_sum); pre = each rank's K1 / K3p / K2 on "
@@ -384,6 +389,12 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if N > 1:
+        def watchdog():
+            time.sleep(args.watchdog)
+            print(json.dumps({"error": f"rank {proc}: no result after {args.watchdog:.0f} s (watchdog)"}), file=sys.stderr,
+                  flush=True)
+            os._exit(3)
+        threading.Thread(target=watchdog, daemon=True).start()
         dist.init_process_group("nccl", device_id=dev)
     dims = synth.PRESETS[wl["model"]]
     g = wl["g"]
@@ -437,7 +448,7 @@ def main():
         obj = [abi.tpla_comm_unique_id() if proc == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         comm = abi.tpla_comm_init(obj[0], N, proc)
-        if not args.no_fused_ar:
+        if args.fused_ar and not args.no_fused_ar:
             try:        # the all-reduce inside the K5 reduce (symmetric window, LSA / NVLS)
                 abi.tpla_comm_enable_fused_allreduce(comm, B * nq * dims.D)
             except abi.TplaError as e:

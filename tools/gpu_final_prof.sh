@@ -10,6 +10,8 @@ PASS=full bash tools/gpu_profile_round.sh > gpurun_out/prof_full_c1.log 2>&1; ec
 cp gpurun_out/prof_full_raw.csv gpurun_out/r02_full_c1_raw.csv; cp gpurun_out/prof_k3_sass.csv gpurun_out/r02_k3_c1_sass.csv
 WL=h8 PASS=full bash tools/gpu_profile_round.sh > gpurun_out/prof_full_h8.log 2>&1; echo "full h8 rc=$?"
 cp gpurun_out/prof_full_raw.csv gpurun_out/r02_full_h8_raw.csv; cp gpurun_out/prof_k3_sass.csv gpurun_out/r02_k3_h8_sass.csv
+if [ -z "$NO_PREFILL" ]; then
 bash tools/gpu_ncu_pf.sh > gpurun_out/prof_pf.log 2>&1; echo "prefill ncu rc=$?"
 timeout 600 python tools/prefill_bench.py --L 1024 4096 --iters 10 > gpurun_out/r02_prefill.jsonl 2>&1; echo "prefill bench rc=$?"
+fi
 ls -la gpurun_out/r02_*

@@ -10,7 +10,7 @@ if [ "$PASS" = "launches" ]; then
   timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/prof_launches.csv \
     $CMD > gpurun_out/prof_ncu.json 2> gpurun_out/prof_ncu.err; echo "ncu rc=$?"
 else
-  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"attn_tc_kernel|skinny_tc_kernel|combine_wuv_kernel|attn_plan_kernel|nt_gemm_kernel" \
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"attn_tc_kernel|skinny_tc_kernel|combine_wuv_kernel|attn_plan_kernel|nt_gemm_kernel|pre_attn_kernel" \
     -c 5 -o gpurun_out/prof_full -f $CMD > gpurun_out/prof_ncu.json 2> gpurun_out/prof_ncu.err; echo "ncu rc=$?"
   ncu -i gpurun_out/prof_full.ncu-rep --page raw --csv > gpurun_out/prof_full_raw.csv 2>/dev/null
   ncu -i gpurun_out/prof_full.ncu-rep --page source --csv --print-source sass -k regex:attn_tc_kernel > gpurun_out/prof_k3_sass.csv 2>/dev/null

@@ -9,7 +9,7 @@ import re
 import sys
 
 NAMES = {"attn_tc_kernel": "K3_attn_tc", "skinny_tc_kernel": "K5_W_O_tc", "combine_wuv_kernel": "K45_combine_W_UV",
-         "attn_plan_kernel": "K3p_attn_plan", "nt_gemm_kernel": "K2_absorb_q", "attn_fwd_causal_kernel": "K8_prefill_fa",
+         "attn_plan_kernel": "K3p_attn_plan", "nt_gemm_kernel": "K2_absorb_q", "pre_attn_kernel": "K3p_K2_pre_attn", "attn_fwd_causal_kernel": "K8_prefill_fa",
          "gemm_tn_kernel": "K9_prefill_gemm"}
 METRICS = [
     ("gpu__time_duration.sum", "duration"),
