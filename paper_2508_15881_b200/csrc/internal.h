@@ -43,7 +43,7 @@ struct SplitPlan {
 // Workspace layout of tpla_decode (byte offsets, all 256-aligned).
 struct WsLayout {
   size_t q_lat;     // bf16 [B, H_loc, W_lat]   (Q'_j)
-  size_t o_part;    // fp32 [B*n_split, H_loc, W_lat]
+  size_t o_part;    // split-K partials: fp32 [B*n_split, H_loc, W_lat] (mma.sync K3), fp16 [segs, ...] (tcgen05 K3)
   size_t ml_part;   // fp32 [B*n_split, H_loc, 2] (m, l)
   size_t o_lat;     // bf16 [B, H_loc, W_lat]   (combined O_j)
   size_t v;         // bf16 [B, H_loc*d_h]
@@ -97,15 +97,16 @@ cudaError_t launch_pre_attn(const Geom& g, const tpla_cache& cache, const int32_
                             cudaStream_t s);
 cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
                                   const int32_t* seq_lens, int B, int n_q, int n_cta, const int32_t* plan,
-                                  float* o_part, float* ml_part, int32_t* meta, cudaStream_t s);
-cudaError_t launch_combine_seg(const Geom& g, int B, const float* o_part, const float* ml_part, const int32_t* meta,
+                                  uint16_t* o_part, float* ml_part, int32_t* meta, cudaStream_t s);
+// (o_part of the persistent K3: fp16 [segs, n_q * H_loc, W_lat] normalised partials O_s / l_s; ml_part (m_s, l_s))
+cudaError_t launch_combine_seg(const Geom& g, int B, const uint16_t* o_part, const float* ml_part, const int32_t* meta,
                                uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s);
 
 // K4 + K5a fused (persistent-K3 partials): v[b, h, :] = combine(partials)[b, h, :] · W^UV'_j[h]ᵀ
 bool combine_wuv_supported(const Geom& g);
 // v_acc != null: write (accumulate: add) v in fp32 there instead of bf16 v, column-chunk-major with
 // v_chunks chunks: element (row b, col c) at ((c / kc) * B*n_q + b) * kc + c % kc, kc = H_loc*d_h / v_chunks
-cudaError_t launch_combine_wuv(const Geom& g, int B, int n_q, const float* o_part, const float* ml_part,
+cudaError_t launch_combine_wuv(const Geom& g, int B, int n_q, const uint16_t* o_part, const float* ml_part,
                                const int32_t* meta, const uint16_t* W_UV, uint16_t* v, cudaStream_t s,
                                float* v_acc = nullptr, bool v_acc_add = false, int v_chunks = 1);
 

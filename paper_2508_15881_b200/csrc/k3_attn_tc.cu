@@ -65,8 +65,8 @@ struct TcArgs {
   const int32_t* block_table;  // [B, max_pages]
   const int32_t* seq_lens;     // [B]
   const int32_t* plan;         // K3p's schedule (plan_ints): per-CTA ranges, first box rows, cum, slen
-  float* o_part;               // [max_segs, H_loc, W_lat]
-  float* ml_part;              // [max_segs, H_loc, 2]
+  uint16_t* o_part;            // fp16 [max_segs, H_loc, W_lat]: the segment's O / l (normalised)
+  float* ml_part;              // [max_segs, H_loc, 2]: (m, l)
   int32_t* meta;               // [B, 2]: first segment id, segment count
   int B, h_loc, h_q, head_begin, page_size, max_pages;
   int n_q;                     // query tokens per sequence (multi-token decode): MMA rows = n_q * h_loc
@@ -827,7 +827,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
                       (m_o == -INFINITY ? 0.f : l_o * ex2(m_o - m_seg));
       const int seg_id = S.seg_base + seg;
       {
-        float* op = a.o_part + ((long)seg_id * n_rows + r) * W_LAT;
+        // the partial leaves normalised (O / l, values of the cache's range) in fp16: half the bytes of
+        // fp32 at 2^-11 relative rounding (R23)
+        uint16_t* op = a.o_part + ((long)seg_id * n_rows + r) * W_LAT;
+        const float inv_l = 1.f / l;
 #pragma unroll 1
         for (int c0 = half * (C::WL / 2); c0 < (half + 1) * (C::WL / 2); c0 += 32) {
           uint32_t ov[32];
@@ -835,9 +838,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           tmem_ld_wait();
           if (row_ok) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(op + c0 + j) = make_float4(__uint_as_float(ov[j]), __uint_as_float(ov[j + 1]),
-                                                                    __uint_as_float(ov[j + 2]), __uint_as_float(ov[j + 3]));
+            for (int j = 0; j < 32; j += 8)
+              *reinterpret_cast<uint4*>(op + c0 + j) =
+                  make_uint4(pack_f16(__uint_as_float(ov[j]) * inv_l, __uint_as_float(ov[j + 1]) * inv_l),
+                             pack_f16(__uint_as_float(ov[j + 2]) * inv_l, __uint_as_float(ov[j + 3]) * inv_l),
+                             pack_f16(__uint_as_float(ov[j + 4]) * inv_l, __uint_as_float(ov[j + 5]) * inv_l),
+                             pack_f16(__uint_as_float(ov[j + 6]) * inv_l, __uint_as_float(ov[j + 7]) * inv_l));
           }
         }
         if (row_ok && half == 0) {
@@ -1021,7 +1027,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       l += red_l[half ^ 1][r];
       const int seg_id = S.seg_base + seg;
       {
-        float* op = a.o_part + ((long)seg_id * n_rows + r) * W_LAT + crank * C::WL;
+        uint16_t* op = a.o_part + ((long)seg_id * n_rows + r) * W_LAT + crank * C::WL;   // (fp16 O / l)
+        const float inv_l = 1.f / l;
 #pragma unroll 1
         for (int c0 = half * (C::WL / 2); c0 < (half + 1) * (C::WL / 2); c0 += 32) {
           uint32_t ov[32];
@@ -1029,9 +1036,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
           tmem_ld_wait();
           if (row_ok) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(op + c0 + j) = make_float4(__uint_as_float(ov[j]), __uint_as_float(ov[j + 1]),
-                                                                    __uint_as_float(ov[j + 2]), __uint_as_float(ov[j + 3]));
+            for (int j = 0; j < 32; j += 8)
+              *reinterpret_cast<uint4*>(op + c0 + j) =
+                  make_uint4(pack_f16(__uint_as_float(ov[j]) * inv_l, __uint_as_float(ov[j + 1]) * inv_l),
+                             pack_f16(__uint_as_float(ov[j + 2]) * inv_l, __uint_as_float(ov[j + 3]) * inv_l),
+                             pack_f16(__uint_as_float(ov[j + 4]) * inv_l, __uint_as_float(ov[j + 5]) * inv_l),
+                             pack_f16(__uint_as_float(ov[j + 6]) * inv_l, __uint_as_float(ov[j + 7]) * inv_l));
           }
         }
         if (row_ok && half == 0 && crank == 0) {
@@ -1060,9 +1070,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tb);
 }
 
-// K4 for the persistent kernel: O = Σ_s 2^{m_s - M} O_s / Σ_s 2^{m_s - M} l_s over the
-// contiguous segment range of sequence b
-__global__ void combine_seg_kernel(const float* __restrict__ o_part, const float* __restrict__ ml_part,
+// K4 for the persistent kernel: O = Σ_s 2^{m_s - M} l_s Ô_s / Σ_s 2^{m_s - M} l_s over the
+// contiguous segment range of sequence b (Ô_s = O_s / l_s, the fp16 partials)
+__global__ void combine_seg_kernel(const uint16_t* __restrict__ o_part, const float* __restrict__ ml_part,
                                    const int32_t* __restrict__ meta, int h_loc, int w_lat,
                                    uint16_t* __restrict__ o_bf16, float* __restrict__ o_f32, float* __restrict__ lse) {
   pdl_trigger();
@@ -1080,9 +1090,10 @@ __global__ void combine_seg_kernel(const float* __restrict__ o_part, const float
   for (int col = threadIdx.x * 4; col < w_lat; col += blockDim.x * 4) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < ns; ++s) {
-      const float w = exp2f(ml_part[((long)(s0 + s) * h_loc + h) * 2] - M);
-      float4 v = *reinterpret_cast<const float4*>(o_part + ((long)(s0 + s) * h_loc + h) * w_lat + col);
-      acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
+      const float* ml = ml_part + ((long)(s0 + s) * h_loc + h) * 2;
+      const float w = exp2f(ml[0] - M) * ml[1];
+      const uint2 u = *reinterpret_cast<const uint2*>(o_part + ((long)(s0 + s) * h_loc + h) * w_lat + col);
+      acc.x += w * f16_lo(u.x); acc.y += w * f16_hi(u.x); acc.z += w * f16_lo(u.y); acc.w += w * f16_hi(u.y);
     }
     acc.x *= inv; acc.y *= inv; acc.z *= inv; acc.w *= inv;
     const long off = ((long)b * h_loc + h) * w_lat + col;
@@ -1321,7 +1332,7 @@ cudaError_t launch_pre_attn(const Geom& g, const tpla_cache& cache, const int32_
 
 cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
                                   const int32_t* seq_lens, int B, int n_q, int n_cta, const int32_t* plan,
-                                  float* o_part, float* ml_part, int32_t* meta, cudaStream_t s) {
+                                  uint16_t* o_part, float* ml_part, int32_t* meta, cudaStream_t s) {
   EncodeFn enc = get_encode();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap map;
@@ -1352,7 +1363,7 @@ cudaError_t launch_decode_attn_tc(const Geom& g, const tpla_cache& cache, const 
   return cudaErrorNotSupported;
 }
 
-cudaError_t launch_combine_seg(const Geom& g, int B, const float* o_part, const float* ml_part, const int32_t* meta,
+cudaError_t launch_combine_seg(const Geom& g, int B, const uint16_t* o_part, const float* ml_part, const int32_t* meta,
                                uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s) {
   dim3 grid(g.h_loc, B);
   int threads = std::min(64, std::max(32, g.w_lat / 4));

@@ -19,7 +19,7 @@ constexpr int kThreads = 32 * kMB;   // one warp per row: the merge is load-late
 constexpr int kSegBatch = 4;        // segments (O row + (m, l)) in flight per lane
 
 struct FArgs {
-  const float* o_part;      // [segs, H_loc, W_lat]
+  const uint16_t* o_part;   // fp16 [segs, n_q * H_loc, W_lat]: normalised partials O_s / l_s
   const float* ml_part;     // [segs, H_loc, 2]
   const int32_t* meta;      // [B, 2] first / last segment of each sequence
   const uint16_t* W_UV;     // [H_loc, d_h, W_lat]
@@ -81,14 +81,12 @@ __global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
         float M = -INFINITY, L = 0.f;
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         for (int sb = s0 + G; sb <= s1; sb += kSegBatch * NG) {
-          float4 x[kSegBatch][2];
+          uint4 x[kSegBatch];                         // 8 fp16 of Ô_s = O_s / l_s
           float2 ml[kSegBatch];
 #pragma unroll
           for (int i = 0; i < kSegBatch; ++i) {       // past s1: reload s1 (no divergent loads), weight 0
             const int sg = sb + i * NG, sc = sg <= s1 ? sg : s1;
-            const float4* src = reinterpret_cast<const float4*>(a.o_part + ((long)sc * n_rows + prow) * a.w_lat + c);
-            x[i][0] = src[0];
-            x[i][1] = src[1];
+            x[i] = *reinterpret_cast<const uint4*>(a.o_part + ((long)sc * n_rows + prow) * a.w_lat + c);
             ml[i] = mlp[(long)sc * n_rows + prow];
           }
           float Mn = M;
@@ -101,10 +99,12 @@ __global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
           for (int e = 0; e < 8; ++e) acc[e] *= r;
 #pragma unroll
           for (int i = 0; i < kSegBatch; ++i) {
-            const float w = sb + i * NG <= s1 ? exp2f(ml[i].x - Mn) : 0.f;
-            L += w * ml[i].y;
-            acc[0] += w * x[i][0].x; acc[1] += w * x[i][0].y; acc[2] += w * x[i][0].z; acc[3] += w * x[i][0].w;
-            acc[4] += w * x[i][1].x; acc[5] += w * x[i][1].y; acc[6] += w * x[i][1].z; acc[7] += w * x[i][1].w;
+            const float wl = (sb + i * NG <= s1 ? exp2f(ml[i].x - Mn) : 0.f) * ml[i].y;   // 2^(m_s - M) l_s
+            L += wl;
+            acc[0] += wl * f16_lo(x[i].x); acc[1] += wl * f16_hi(x[i].x);
+            acc[2] += wl * f16_lo(x[i].y); acc[3] += wl * f16_hi(x[i].y);
+            acc[4] += wl * f16_lo(x[i].z); acc[5] += wl * f16_hi(x[i].z);
+            acc[6] += wl * f16_lo(x[i].w); acc[7] += wl * f16_hi(x[i].w);
           }
           M = Mn;
         }
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
 
 bool combine_wuv_supported(const Geom& g) { return g.d_h % 8 == 0 && g.w_lat % 64 == 0 && g.w_lat <= 512; }
 
-cudaError_t launch_combine_wuv(const Geom& g, int B, int n_q, const float* o_part, const float* ml_part,
+cudaError_t launch_combine_wuv(const Geom& g, int B, int n_q, const uint16_t* o_part, const float* ml_part,
                                const int32_t* meta, const uint16_t* W_UV, uint16_t* v, cudaStream_t s,
                                float* v_acc, bool v_acc_add, int v_chunks) {
   FArgs a{o_part, ml_part, meta, W_UV, v, B, g.h_loc, g.w_lat, g.d_h, n_q, v_acc, v_acc_add ? 1 : 0, v_chunks};

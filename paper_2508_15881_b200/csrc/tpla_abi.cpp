@@ -319,13 +319,14 @@ static cudaError_t run_attention(const Geom& g, const tpla_cache& cache, const u
   auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
   cudaError_t e;
   if (use_tc_attention(g, B)) {
+    auto* o16 = reinterpret_cast<uint16_t*>(base + L.o_part);       // (fp16 partials)
     auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
     auto* plan = reinterpret_cast<int32_t*>(base + L.plan);
     e = launch_attn_plan(g, cache, seq_lens, B, L.n_cta, plan, s);
     if (e != cudaSuccess) return e;
-    e = launch_decode_attn_tc(g, cache, q_lat, q_pe, seq_lens, B, 1, L.n_cta, plan, o_part, ml_part, meta, s);
+    e = launch_decode_attn_tc(g, cache, q_lat, q_pe, seq_lens, B, 1, L.n_cta, plan, o16, ml_part, meta, s);
     if (e != cudaSuccess || (!o_bf16 && !o_f32 && !lse)) return e;   // no output requested: K3 alone
-    return launch_combine_seg(g, B, o_part, ml_part, meta, o_bf16, o_f32, lse, s);
+    return launch_combine_seg(g, B, o16, ml_part, meta, o_bf16, o_f32, lse, s);
   }
   SplitPlan sp = choose_split(B, max_seq_len);
   e = launch_decode_attn(g, cache, q_lat, q_pe, seq_lens, B, sp, o_part, ml_part, s);
@@ -646,7 +647,7 @@ tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const
   if (tc_path) {
     // K3: per-shard split-K flash decoding (Eq. tpla_softmax_one_device) -> partials;
     // K4 + K5a fused: merge the partials of each (b, h) into O_j and apply W^UV'_j
-    auto* o_part = reinterpret_cast<float*>(base + L.o_part);
+    auto* o_part = reinterpret_cast<uint16_t*>(base + L.o_part);   // (fp16 partials)
     auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
     auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
     e = launch_decode_attn_tc(g, *cache, q_lat, static_cast<const uint16_t*>(q_pe), seq_lens, B, n_q, L.n_cta,
@@ -804,7 +805,7 @@ tpla_status tpla_decode_v(const tpla_config* cfg, const tpla_weights* w, const t
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(ws);
   auto* q_lat = reinterpret_cast<uint16_t*>(base + L.q_lat);
-  auto* o_part = reinterpret_cast<float*>(base + L.o_part);
+  auto* o_part = reinterpret_cast<uint16_t*>(base + L.o_part);     // (fp16 partials)
   auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
   auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
   const auto* qn = static_cast<const uint16_t*>(q_nope);
