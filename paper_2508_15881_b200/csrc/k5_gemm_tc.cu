@@ -43,7 +43,16 @@ struct GCfg {
   static constexpr int A_BYTES = kTM * 128;            // 16 KB
   static constexpr int B_BYTES = NP * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int NST = std::min(12, (200 * 1024) / STAGE);
+#ifndef TPLA_K5_SMEM_KB
+#define TPLA_K5_SMEM_KB 200
+#endif
+// Ring depth: at most 6 stages (A/B, tools/gpu_ab_k.sh: 6 / 8 / 10 / 11 stages of 20 KB at B <= 32 —
+// K5 43.5 / 44.0 / 45.5 / 45.5 us per c1 step, 42.0 / 42.1 / 44.9 / 45.5 at batch 1; ncu cold 40.5 us
+// at 8 against 43.0 at 10: ~120 KB in flight per SM already covers the HBM latency)
+#ifndef TPLA_K5_MAX_NST
+#define TPLA_K5_MAX_NST 6
+#endif
+  static constexpr int NST = std::min(TPLA_K5_MAX_NST, (TPLA_K5_SMEM_KB * 1024) / STAGE);
   static constexpr int SMEM = 1024 + NST * STAGE;
   static constexpr int TMEM_COLS = 2 * NP < 32 ? 32 : 2 * NP;
 };
