@@ -148,7 +148,13 @@ struct Cfg {
   static constexpr int STAGE_BYTES = NBOX * BOX_BYTES;
   static constexpr int QPE_BYTES = 128 * 128;         // q^PE A operand [128 rows x 64] bf16
   static constexpr int XCH_BYTES = PAIR ? 2 * 8 * 32 * CH * 4 : 0;   // PAIR: peer's partial logits + ours to send
-  static constexpr int NST = std::min(8, (220 * 1024 - QPE_BYTES - XCH_BYTES) / STAGE_BYTES);
+  // Ring depth, A/B over 3-6 stages (tools/gpu_ab_k.sh): 4 x 40 KB at W_lat = 256 (c1 K3 244.0 ->
+  // 242.6 us per step, against the 5 that fit), 5 x 32 KB at W_lat <= 128 (h8 499.5 -> 496.0, c3
+  // 847 -> 843, against 6; 4 is slower there, 3 slower everywhere); the CTA pair keeps what fits.
+#ifndef TPLA_K3_MAX_NST
+#define TPLA_K3_MAX_NST (PAIR ? 8 : W_LAT == 256 ? 4 : 5)
+#endif
+  static constexpr int NST = std::min(TPLA_K3_MAX_NST, (220 * 1024 - QPE_BYTES - XCH_BYTES) / STAGE_BYTES);
   static constexpr int SMEM = 1024 + QPE_BYTES + XCH_BYTES + NST * STAGE_BYTES;
   // TMEM columns
   static constexpr int O_COL = 0;
