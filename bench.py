@@ -739,7 +739,11 @@ def main():
         ev_out = [torch.cuda.Event() for _ in range(2)]
         barrier()
         torch.cuda.synchronize()
+        # (a second of idle first: the sustained-clock replays above hold the board at its power cap, and
+        # the e2e region should see the same clocks as the main timed region; its own clocks are reported)
+        time.sleep(1.0)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ce = ClockSampler(local, period_s=0.002).__enter__()
         e0.record(stream)
         cs_in.wait_event(e0)
         for i in range(n_e2e):
@@ -764,6 +768,7 @@ def main():
         ev_out[(n_e2e - 1) & 1].synchronize()
         e1.record(cs_out)
         torch.cuda.synchronize()
+        ce.__exit__(None, None, None)
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1))
         if args.e2e_diag and g1[0] is not None:
@@ -802,7 +807,8 @@ def main():
         e2e = {"value": B * nq * n_e2e / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": n_e2e, "ms_per_step": ems / n_e2e,
                "pipeline": "double-buffered: H2D of step i and D2H of step i-1 on copy streams, "
-                           "overlapping compute; host waits for every step's output"}
+                           "overlapping compute; host waits for every step's output",
+               "clocks": ce.summary(ems / 1e3)}
 
     # ---- parity of this run's own step against the fp64 oracle, and the oracle timed (cpu_baseline)
     cpu = None
