@@ -957,3 +957,88 @@ def test_c_example_runs_on_gpu(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "decode_step OK" in r.stdout and "K3 path: 1" in r.stdout, r.stdout
+
+
+# ----------------------------------------------------------------------------- guard bands
+# compute-sanitizer is closed on this pool (profiles/r02_sanitizer_pool_closed.log), so out-of-bounds
+# WRITES are checked directly: every buffer a call writes sits between canary regions, the paged cache
+# is pre-filled with a canary, and after the calls every byte outside the documented output extents
+# must still hold its canary.
+def _guarded(shape, dtype, d, fill):
+    g = 4096 // torch.tensor([], dtype=dtype).element_size()
+    n = int(np.prod(shape))
+    full = torch.full((n + 2 * g,), fill, dtype=dtype, device=d)
+    return full, full[g:g + n].view(shape), g
+
+
+def _canary_intact(full, g, fill):
+    return bool((full[:g] == fill).all()) and bool((full[-g:] == fill).all())
+
+
+@pytest.mark.parametrize("k,g,S_list,n_q", [(2, 2, [300, 77, 1025], 1), (8, 8, [129, 64, 700, 1], 1),
+                                            (4, 2, [200, 513], 2)])
+def test_no_writes_outside_outputs(k, g, S_list, n_q):
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    B = len(S_list)
+    xf, sseed, U, U32, alpha = transform_inputs("hadamard", dims, 3, g)
+    w = synth.gen_weights(dims, 5)
+    q, qpe = synth.gen_queries(dims, B * n_q, 6)
+    q = bf16_from_bits(q, d).view(B, n_q, dims.h_q, dims.d_h) if n_q > 1 else bf16_from_bits(q, d)
+    qpe = bf16_from_bits(qpe, d).view(B, n_q, dims.h_q, dims.d_r) if n_q > 1 else bf16_from_bits(qpe, d)
+    lens = torch.tensor(S_list, dtype=torch.int32, device=d)
+    CANARY16 = 0x1234                                   # a finite bf16 (the cache's unused rows must be finite)
+    for rid in range(k):
+        r = TplaRank(spec_of(dims), k=k, g=g, rank=rid, batch=B, max_seq_len=max(S_list), device=d, extra_pages=3,
+                     n_q=n_q)
+        r.convert(w.W_UK, w.W_UV, w.gamma, w.W_O, xform=xf, sign_seed=sseed, alpha=alpha,
+                  mu=np.asarray(alpha, float))
+        r.cache_buf.view(torch.int16).fill_(CANARY16)
+        ws_full, r.ws, gw = _guarded((r.ws_bytes,), torch.uint8, d, 0xA5)
+        for b, S in enumerate(S_list):
+            ck = bf16_from_bits(synth.gen_raw_ckv(dims, S, 7, b), d)
+            kp = bf16_from_bits(synth.gen_kpe(dims, S, 7, b), d)
+            r.append(ck, kp, torch.full((S,), b, dtype=torch.int32, device=d),
+                     torch.arange(S, dtype=torch.int32, device=d), abi.RMS_EXACT)
+        R = B * n_q
+        y_full, y, gy = _guarded((R, dims.D), torch.float32, d, -7.0)
+        o_full, out, go = _guarded((R, dims.D), torch.int16, d, 0x5555)
+        if n_q > 1:
+            r.decode_mtp(q, qpe, lens, y, out.view(torch.bfloat16))
+        else:
+            r.decode(q, qpe, lens, y, out.view(torch.bfloat16))
+            va_full, va, gv = _guarded(r.v_acc_shape(R, 1), torch.float32, d, -9.0)
+            r.decode_v(q, qpe, lens, va)
+            r.project_out(va, y, out.view(torch.bfloat16), accumulate=True)
+            torch.cuda.synchronize()
+            assert _canary_intact(va_full, gv, -9.0)
+        torch.cuda.synchronize()
+        assert _canary_intact(ws_full, gw, 0xA5), "workspace overrun"
+        assert _canary_intact(y_full, gy, -7.0) and _canary_intact(o_full, go, 0x5555), "output overrun"
+        # cache: only rows [0, S_b) of sequence b's pages were written; the rest (and the spare pages) kept
+        cb = r.cache_buf.view(torch.int16)
+        written = torch.zeros(cb.shape[:2], dtype=torch.bool, device=d)
+        for b, S in enumerate(S_list):
+            for t0 in range(0, S, r.page_size):
+                pg = int(r.block_table_host[b, t0 // r.page_size])
+                written[pg, :min(r.page_size, S - t0)] = True
+        assert bool((cb[~written] == CANARY16).all()), "cache rows outside the appended positions changed"
+        assert bool((cb[written][:, r.plan.row_width:] == CANARY16).all()), "row padding changed"
+
+
+def test_no_writes_outside_prefill_outputs():
+    from paper_2508_15881_b200.runtime import PrefillRank
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    L = 333
+    w = synth.gen_weights(dims, 8)
+    q, qpe = synth.gen_queries(dims, L, 9)
+    args = [bf16_from_bits(x, d) for x in (synth.gen_raw_ckv(dims, L, 10, 0), synth.gen_kpe(dims, L, 10, 0), q, qpe)]
+    pr = PrefillRank(spec_of(dims), k=2, rank=0, max_len=L, device=d)
+    pr.convert(w.W_UK, w.W_UV, w.gamma, w.W_O)
+    ws_full, pr.ws, gw = _guarded((pr.ws_bytes,), torch.uint8, d, 0xA5)
+    y_full, y, gy = _guarded((L, dims.D), torch.float32, d, -7.0)
+    o_full, out, go = _guarded((L, dims.D), torch.int16, d, 0x5555)
+    pr.forward(*args, y, out.view(torch.bfloat16))
+    torch.cuda.synchronize()
+    assert _canary_intact(ws_full, gw, 0xA5) and _canary_intact(y_full, gy, -7.0) and _canary_intact(o_full, go, 0x5555)
