@@ -1001,6 +1001,22 @@ def test_no_writes_outside_outputs(k, g, S_list, n_q):
             r.append(ck, kp, torch.full((S,), b, dtype=torch.int32, device=d),
                      torch.arange(S, dtype=torch.int32, device=d), abi.RMS_EXACT)
         R = B * n_q
+        # reads: the same decode with NaN in every workspace byte and NaN bf16 around the queries must give
+        # the bits of a run on a zeroed workspace (no kernel reads scratch it did not write first, nor
+        # past its inputs)
+        NAN16 = 0x7FC0
+        qg_full, qg, _ = _guarded(tuple(q.shape), torch.int16, d, NAN16)
+        pg_full, pg, _ = _guarded(tuple(qpe.shape), torch.int16, d, NAN16)
+        qg.copy_(q.view(torch.int16))
+        pg.copy_(qpe.view(torch.int16))
+        y_ref = torch.zeros((R, dims.D), dtype=torch.float32, device=d)
+        y_nan = torch.zeros_like(y_ref)
+        r.ws.zero_()
+        (r.decode_mtp if n_q > 1 else r.decode)(q, qpe, lens, y_ref)
+        r.ws.fill_(0xFF)
+        (r.decode_mtp if n_q > 1 else r.decode)(qg.view(torch.bfloat16), pg.view(torch.bfloat16), lens, y_nan)
+        torch.cuda.synchronize()
+        assert torch.isfinite(y_ref).all() and torch.equal(y_nan, y_ref), "read of unwritten scratch or past an input"
         y_full, y, gy = _guarded((R, dims.D), torch.float32, d, -7.0)
         o_full, out, go = _guarded((R, dims.D), torch.int16, d, 0x5555)
         if n_q > 1:
