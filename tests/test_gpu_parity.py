@@ -1058,3 +1058,9 @@ def test_no_writes_outside_prefill_outputs():
     pr.forward(*args, y, out.view(torch.bfloat16))
     torch.cuda.synchronize()
     assert _canary_intact(ws_full, gw, 0xA5) and _canary_intact(y_full, gy, -7.0) and _canary_intact(o_full, go, 0x5555)
+    # reads: NaN in every workspace byte gives the same bits (no read of unwritten scratch)
+    y2 = torch.empty_like(y)
+    pr.ws.fill_(0xFF)
+    pr.forward(*args, y2)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y).all() and torch.equal(y2, y)
