@@ -1064,3 +1064,21 @@ def test_no_writes_outside_prefill_outputs():
     pr.forward(*args, y2)
     torch.cuda.synchronize()
     assert torch.isfinite(y).all() and torch.equal(y2, y)
+
+
+# ----------------------------------------------------------------------------- seeded random configurations
+_KG = [(1, 1), (2, 1), (2, 2), (4, 2), (4, 4), (8, 2), (8, 4), (8, 8)]
+
+
+@pytest.mark.parametrize("case", range(int(__import__("os").environ.get("TPLA_FUZZ_CASES", "20"))))
+def test_e2e_parity_random_configs(case):
+    """Seeded random (model, k, g, transform, batch, ragged lengths, W^O mode) drawn per case: the
+    production decode (K1, fused K3p + K2, K3 incl. the g = 1 CTA pair, K45, K5) against the oracle."""
+    rng = np.random.default_rng(1000 + case)
+    dname = ["dsv3", "kimi"][int(rng.integers(2))]
+    k, g = _KG[int(rng.integers(len(_KG)))]
+    kind = ["identity", "hadamard", "pca"][int(rng.integers(3))] if g > 1 else "identity"
+    B = int(rng.integers(1, 41))
+    S_list = [int(x) for x in rng.integers(1, 1500, size=B)]
+    wo = "shared" if g > 1 and rng.integers(2) else "rank"
+    e2e_case(dev(), synth.PRESETS[dname], k, g, kind, S_list, seed=case, wo=wo)
