@@ -1082,3 +1082,26 @@ def test_e2e_parity_random_configs(case):
     S_list = [int(x) for x in rng.integers(1, 1500, size=B)]
     wo = "shared" if g > 1 and rng.integers(2) else "rank"
     e2e_case(dev(), synth.PRESETS[dname], k, g, kind, S_list, seed=case, wo=wo)
+
+
+@pytest.mark.parametrize("case", range(int(__import__("os").environ.get("TPLA_FUZZ_CASES_MTP", "8"))))
+def test_mtp_parity_random_configs(case):
+    """Seeded random multi-token decode shapes (n_q * H_loc <= 128) against the per-token oracle."""
+    rng = np.random.default_rng(2000 + case)
+    dname = ["dsv3", "kimi"][int(rng.integers(2))]
+    dims = synth.PRESETS[dname]
+    choices = [(k, g, n) for k, g in _KG for n in (2, 3, 4) if g > 1 and n * dims.h_q // (k // g) <= 128]
+    k, g, n_q = choices[int(rng.integers(len(choices)))]
+    B = int(rng.integers(1, 17))
+    S_list = [int(x) for x in rng.integers(n_q, 1200, size=B)]
+    mtp_case(dev(), dims, k, g, n_q, S_list, seed=case, kind=["identity", "hadamard"][int(rng.integers(2))])
+
+
+@pytest.mark.parametrize("case", range(int(__import__("os").environ.get("TPLA_FUZZ_CASES_PF", "4"))))
+def test_prefill_mla_forward_random_configs(case):
+    """Seeded random prompt lengths and head splits of the non-absorbed prefill, sampled positions."""
+    rng = np.random.default_rng(3000 + case)
+    dname = ["dsv3", "kimi"][int(rng.integers(2))]
+    k = [1, 2, 4][int(rng.integers(3))]
+    L = int(rng.integers(1, 1400))
+    prefill_mla_forward_case(dev(), synth.PRESETS[dname], k, L, sample=min(L, 24), seed=case)
