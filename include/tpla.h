@@ -323,8 +323,8 @@ tpla_status tpla_decode_mtp(const tpla_config* cfg, const tpla_weights* w, const
 /* K3 + K4 only (attention of one shard, Eq. tpla_softmax_one_device without W^VO):
  *   q_lat: device bf16 [B, H_loc, W_lat] (= Q'_j, mu_j included); q_pe: device bf16 [B, h_q, d_r]
  *   (all heads); O: device fp32 [B, H_loc, W_lat] = Σ_t p_t ĉ_{j,t};  lse: device fp32 [B, H_loc]
- *   or NULL: log Σ_t exp(s_t) (natural log, s_t including sm_scale).  O = lse = NULL runs K3 alone
- *   (its partials stay in the workspace): used to time the attention kernel by itself. */
+ *   or NULL: log Σ_t exp(s_t) (natural log, s_t including sm_scale).  O = lse = NULL skips K4 (the
+ *   partials stay in the workspace).  On the tcgen05 path K3's schedule kernel K3p runs first. */
 tpla_status tpla_decode_attention(const tpla_config* cfg, const tpla_cache* cache, const void* q_lat,
                                   const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t max_seq_len,
                                   void* ws, size_t ws_bytes, float* O, float* lse, void* stream);
@@ -346,6 +346,14 @@ tpla_status tpla_comm_init(tpla_comm** out, const void* unique_id128, int32_t wo
  * NVLink in rank order) — no separate ncclAllReduce or cast launch.  TPLA_FUSED_AR=0 disables it per
  * process, =unicast forbids the multicast.  TPLA_ERR_UNSUPPORTED if the loaded NCCL has no device API
  * matching the headers (NCCL 2.28).  tpla_comm_fused_allreduce_mode: 0 off, 1 peer loads, 2 multicast. */
+/* tpla_decode_attention with flags.  TPLA_ATTN_REUSE_PLAN: no K3p — K3 reuses the schedule that a
+ * completed tpla_decode_attention on the same workspace left there (same cfg, cache, seq_lens contents,
+ * B and max_seq_len; the caller guarantees it), so O = lse = NULL runs K3 ALONE (to time the attention
+ * kernel by itself).  Requires the tcgen05 K3 (TPLA_ERR_UNSUPPORTED otherwise). */
+enum { TPLA_ATTN_REUSE_PLAN = 1 };
+tpla_status tpla_decode_attention_ex(const tpla_config* cfg, const tpla_cache* cache, const void* q_lat,
+                                     const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t max_seq_len,
+                                     void* ws, size_t ws_bytes, float* O, float* lse, int32_t flags, void* stream);
 /* Which attention kernel tpla_decode / tpla_decode_v / tpla_decode_attention run for this shape
  * (validated first; a status < 0 is -(tpla_status) of the failed validation): 1 = the tcgen05
  * persistent K3 (d_r = 64, W_lat in {64, 128, 256, 512}, B <= 512), 0 = the mma.sync K3 that serves

@@ -37,6 +37,7 @@ XFORM_IDENTITY, XFORM_HADAMARD, XFORM_PCA = 0, 1, 2
 RMS_SLICED, RMS_EXACT, RMS_NONE = 0, 1, 2
 DECODE_ACCUMULATE = 1
 DECODE_STAGE_PRE, DECODE_STAGE_ATTN = 2, 4
+ATTN_REUSE_PLAN = 1
 
 _STATUS = {0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "DIVISIBILITY", 4: "CAPACITY", 5: "CUDA", 6: "NCCL",
            7: "UNSUPPORTED"}
@@ -110,6 +111,8 @@ _SIGS = {
                          _I, _P, _S, _P, _P, _I, _P, _P], _I),
     "tpla_decode_attention": ([C.POINTER(tpla_config), C.POINTER(tpla_cache), _P, _P, _P, _I, _I, _P, _S, _P, _P,
                                _P], _I),
+    "tpla_decode_attention_ex": ([C.POINTER(tpla_config), C.POINTER(tpla_cache), _P, _P, _P, _I, _I, _P, _S, _P, _P,
+                                  _I, _P], _I),
     "tpla_prefill_weights_bytes": ([C.POINTER(tpla_config), C.POINTER(_S), C.POINTER(_S), C.POINTER(_S)], _I),
     "tpla_convert_prefill_weights": ([C.POINTER(tpla_config), _P, _P, _P, _P, C.POINTER(tpla_prefill_weights), _P],
                                      _I),
@@ -317,6 +320,13 @@ def tpla_decode_attention(cfg, cache, q_lat, q_pe, seq_lens, B, max_seq_len, ws,
     _check(_lib.tpla_decode_attention(C.byref(cfg), C.byref(cache), _ptr(q_lat), _ptr(q_pe), _ptr(seq_lens), B,
                                       max_seq_len, _ptr(ws), ws_bytes, _ptr(O), _ptr(lse), _ptr(stream)),
            "tpla_decode_attention")
+
+
+def tpla_decode_attention_ex(cfg, cache, q_lat, q_pe, seq_lens, B, max_seq_len, ws, ws_bytes, O, lse=None, flags=0,
+                             stream=0):
+    _check(_lib.tpla_decode_attention_ex(C.byref(cfg), C.byref(cache), _ptr(q_lat), _ptr(q_pe), _ptr(seq_lens), B,
+                                         max_seq_len, _ptr(ws), ws_bytes, _ptr(O), _ptr(lse), flags, _ptr(stream)),
+           "tpla_decode_attention_ex")
 
 
 def tpla_comm_unique_id() -> bytes:

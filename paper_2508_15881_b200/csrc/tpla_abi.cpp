@@ -314,7 +314,7 @@ static bool use_tc_attention(const Geom& g, int B) {
 
 static cudaError_t run_attention(const Geom& g, const tpla_cache& cache, const uint16_t* q_lat, const uint16_t* q_pe,
                                  const int32_t* seq_lens, int B, int max_seq_len, const WsLayout& L, char* base,
-                                 uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s) {
+                                 uint16_t* o_bf16, float* o_f32, float* lse, cudaStream_t s, bool reuse_plan = false) {
   auto* o_part = reinterpret_cast<float*>(base + L.o_part);
   auto* ml_part = reinterpret_cast<float*>(base + L.ml_part);
   cudaError_t e;
@@ -322,8 +322,7 @@ static cudaError_t run_attention(const Geom& g, const tpla_cache& cache, const u
     auto* o16 = reinterpret_cast<uint16_t*>(base + L.o_part);       // (fp16 partials)
     auto* meta = reinterpret_cast<int32_t*>(base + L.meta);
     auto* plan = reinterpret_cast<int32_t*>(base + L.plan);
-    e = launch_attn_plan(g, cache, seq_lens, B, L.n_cta, plan, s);
-    if (e != cudaSuccess) return e;
+    if (!reuse_plan && (e = launch_attn_plan(g, cache, seq_lens, B, L.n_cta, plan, s)) != cudaSuccess) return e;
     e = launch_decode_attn_tc(g, cache, q_lat, q_pe, seq_lens, B, 1, L.n_cta, plan, o16, ml_part, meta, s);
     if (e != cudaSuccess || (!o_bf16 && !o_f32 && !lse)) return e;   // no output requested: K3 alone
     return launch_combine_seg(g, B, o16, ml_part, meta, o_bf16, o_f32, lse, s);
@@ -1058,6 +1057,12 @@ tpla_status tpla_prefill_mla_forward(const tpla_config* cfg, const tpla_prefill_
 tpla_status tpla_decode_attention(const tpla_config* cfg, const tpla_cache* cache, const void* q_lat,
                                   const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t max_seq_len,
                                   void* ws, size_t ws_bytes, float* O, float* lse, void* stream) {
+  return tpla_decode_attention_ex(cfg, cache, q_lat, q_pe, seq_lens, B, max_seq_len, ws, ws_bytes, O, lse, 0, stream);
+}
+
+tpla_status tpla_decode_attention_ex(const tpla_config* cfg, const tpla_cache* cache, const void* q_lat,
+                                     const void* q_pe, const int32_t* seq_lens, int32_t B, int32_t max_seq_len,
+                                     void* ws, size_t ws_bytes, float* O, float* lse, int32_t flags, void* stream) {
   Geom g{};
   tpla_status st = make_geom(cfg, &g);
   if (st) return st;
@@ -1065,12 +1070,16 @@ tpla_status tpla_decode_attention(const tpla_config* cfg, const tpla_cache* cach
   if (!q_lat || !ws) return fail(TPLA_ERR_INVALID_ARG, "NULL q_lat/ws");
   if (!O && lse) return fail(TPLA_ERR_INVALID_ARG, "lse requires O");
   if (!aligned16(q_lat) || !aligned16(ws)) return fail(TPLA_ERR_INVALID_ARG, "misaligned pointer");
+  if (flags & ~int32_t(TPLA_ATTN_REUSE_PLAN)) return fail(TPLA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  const bool reuse = (flags & TPLA_ATTN_REUSE_PLAN) != 0;
+  if (reuse && !use_tc_attention(g, B))
+    return fail(TPLA_ERR_UNSUPPORTED, "TPLA_ATTN_REUSE_PLAN needs the tcgen05 K3 (no schedule otherwise)");
   WsLayout L = ws_layout(g, B, 1, max_seq_len);
   if (ws_bytes < L.total) return fail(TPLA_ERR_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* base = static_cast<char*>(ws);
   cudaError_t e = run_attention(g, *cache, static_cast<const uint16_t*>(q_lat), static_cast<const uint16_t*>(q_pe),
-                                seq_lens, B, max_seq_len, L, base, nullptr, O, lse, s);
+                                seq_lens, B, max_seq_len, L, base, nullptr, O, lse, s, reuse);
   if (e != cudaSuccess) return cuda_fail(e, "K3/K4 decode attention");
   return ok();
 }

@@ -212,10 +212,12 @@ class TplaRank:
         abi.tpla_project_out_sum(self.cfg, self.weights, list(v_list), R, n_chunks, chunk, self.ws, self.ws_bytes, y, out,
                                  abi.DECODE_ACCUMULATE if accumulate else 0, comm, stream_ptr(stream))
 
-    def decode_attention(self, q_lat, q_pe, seq_lens, O, lse=None, *, B: int | None = None, stream=None):
+    def decode_attention(self, q_lat, q_pe, seq_lens, O, lse=None, *, B: int | None = None, reuse_plan=False,
+                         stream=None):
+        """reuse_plan: K3 without its schedule kernel, on the plan a previous call on this workspace left."""
         B = int(q_lat.shape[0]) if B is None else B
-        abi.tpla_decode_attention(self.cfg, self.cache, q_lat, q_pe, seq_lens, B, self.max_seq_len, self.ws,
-                                  self.ws_bytes, O, lse, stream_ptr(stream))
+        abi.tpla_decode_attention_ex(self.cfg, self.cache, q_lat, q_pe, seq_lens, B, self.max_seq_len, self.ws,
+                                     self.ws_bytes, O, lse, abi.ATTN_REUSE_PLAN if reuse_plan else 0, stream_ptr(stream))
 
     # ---- host view of the cache (tests)
     def cache_rows_bits(self, b: int, n: int) -> np.ndarray:

@@ -247,3 +247,19 @@ def test_header_is_c99():
     r = subprocess.run(["gcc", "-std=c99", "-pedantic", "-Wall", "-Wextra", "-Werror", "-I" + os.path.join(ROOT, "include"),
                         "-x", "c", "-fsyntax-only", "-"], input=src, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_decode_attention_ex_host_checks():
+    """tpla_decode_attention_ex: unknown flags -> INVALID_ARG; TPLA_ATTN_REUSE_PLAN off the tcgen05 K3
+    (here d_r = 16: the mma.sync kernel, which has no schedule to reuse) -> UNSUPPORTED; nothing launched."""
+    c = cfg(d_r=16)
+    cache = abi.tpla_cache(1 << 20, 1 << 20, 16, 64, 4, 320, 2)
+    n_before = abi.tpla_launch_count()
+    with pytest.raises(abi.TplaError) as ei:
+        abi.tpla_decode_attention_ex(c, cache, 1 << 20, 1 << 20, 1 << 20, 2, 256, 1 << 20, 1 << 30, None, None, 4)
+    assert ei.value.status == abi.ERR_INVALID_ARG
+    with pytest.raises(abi.TplaError) as ei:
+        abi.tpla_decode_attention_ex(c, cache, 1 << 20, 1 << 20, 1 << 20, 2, 256, 1 << 20, 1 << 30, None, None,
+                                     abi.ATTN_REUSE_PLAN)
+    assert ei.value.status == abi.ERR_UNSUPPORTED
+    assert abi.tpla_launch_count() == n_before

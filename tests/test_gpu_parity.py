@@ -1105,3 +1105,26 @@ def test_prefill_mla_forward_random_configs(case):
     k = [1, 2, 4][int(rng.integers(3))]
     L = int(rng.integers(1, 1400))
     prefill_mla_forward_case(dev(), synth.PRESETS[dname], k, L, sample=min(L, 24), seed=case)
+
+
+@pytest.mark.parametrize("k,g", [(2, 2), (8, 8), (2, 1)])
+def test_decode_attention_reuse_plan_bit_identical(k, g):
+    """TPLA_ATTN_REUSE_PLAN (K3 without K3p, on the schedule the previous call left in the workspace, as
+    the bench's K3-alone timings use it) gives the bits of the full call."""
+    d = dev()
+    dims = synth.PRESETS["dsv3"]
+    S_list = [1000, 3, 257]
+    B = len(S_list)
+    r = TplaRank(spec_of(dims), k=k, g=g, rank=k - 1, batch=B, max_seq_len=max(S_list), device=d, page_perm_seed=3)
+    gen = torch.Generator(device=d)
+    gen.manual_seed(11)
+    r.cache_buf[..., :r.plan.row_width].normal_(generator=gen)
+    q_lat = torch.randn((B, r.plan.h_loc, r.plan.w_lat), generator=gen, device=d).to(torch.bfloat16)
+    q_pe = torch.randn((B, dims.h_q, dims.d_r), generator=gen, device=d).to(torch.bfloat16)
+    lens = torch.tensor(S_list, dtype=torch.int32, device=d)
+    O1 = torch.empty((B, r.plan.h_loc, r.plan.w_lat), dtype=torch.float32, device=d)
+    O2 = torch.full_like(O1, float("nan"))
+    r.decode_attention(q_lat, q_pe, lens, O1)
+    r.decode_attention(q_lat, q_pe, lens, O2, reuse_plan=True)
+    torch.cuda.synchronize()
+    assert torch.isfinite(O1).all() and torch.equal(O1, O2)
