@@ -17,6 +17,7 @@
 //
 // Warp roles (384 threads): w0 TMA, w1 MMA, w2 TMEM allocator, w4-w11 epilogue.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -27,7 +28,7 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kM = 128, kN = 256, kK = 64;
+constexpr int kM = 128, kN = 256, kK = 64;      // kN: the largest token tile (runtime a.tn <= kN, 32 | tn)
 constexpr int kMT = 2;                        // weight row tiles per CTA (MMA M = 128 each)
 constexpr int kWBytes = kM * 128;             // 16 KB per row tile
 constexpr int kXBytes = kN * 128;             // 32 KB
@@ -39,6 +40,7 @@ struct G9Args {
   float* y;           // [L, N] fp32 or null
   uint16_t* out;      // [L, N] bf16 or null
   int N, L, k_steps, n_tt, n_rt, accumulate;
+  int tn;             // tokens per tile (MMA N): chosen per launch against the wave quantisation
 };
 
 __global__ void __launch_bounds__(384, 1)
@@ -72,15 +74,15 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ C
         const int st = ks % kStages;
         mbar_wait(&empty[st], ((ks / kStages) & 1) ^ 1);
         uint8_t* dst = smem + st * kStage;
-        mbar_arrive_expect_tx(&full[st], n_mt * kWBytes + kXBytes);
+        mbar_arrive_expect_tx(&full[st], n_mt * kWBytes + a.tn * 128);
         for (int m = 0; m < n_mt; ++m)
           tma_load_2d(dst + m * kWBytes, &mw, 0, ((rp * kMT + m) * a.k_steps + ks) * kM, &full[st], kEvictNormal);
-        tma_load_2d(dst + kMT * kWBytes, &mx, ks * kK, tt * kN, &full[st], kEvictNormal);
+        tma_load_2d(dst + kMT * kWBytes, &mx, ks * kK, tt * a.tn, &full[st], kEvictNormal);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16(kM, kN, false, false);
+    const uint32_t idesc = idesc_bf16(kM, a.tn, false, false);
     constexpr uint32_t hi_k = desc_sw128_hi(1024);
     const uint32_t s0 = smem_addr(smem);
     for (int ks = 0; ks < a.k_steps; ++ks) {
@@ -116,7 +118,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ C
     uint16_t* stg16 = reinterpret_cast<uint16_t*>(smem + 8 * 2 * 4096) + wi * 2 * 1024;   // 2 x [32 x 32] bf16
     const int n0 = (rp * kMT + m) * kM + q4 * 32;
 #pragma unroll 1
-    for (int c = 0; c < kN / 32; ++c) {
+    for (int c = 0; c < a.tn / 32; ++c) {
       uint32_t d[32];
       tmem_ld32(lane_base + 32 * c, d);
       tmem_ld_wait();
@@ -132,7 +134,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ C
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        const int t0 = tt * kN + 32 * c;
+        const int t0 = tt * a.tn + 32 * c;
         if (a.y) {
           if (a.accumulate) tma_reduce_add_2d(&my, n0, t0, bf);
           else tma_store_2d(&my, n0, t0, bf);
@@ -174,16 +176,49 @@ bool map2d(CUtensorMap* m, const void* base, long cols, long rows, long ld, int 
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+int sm_count9() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 }  // namespace
 
 bool gemm_tn_supported(int N, int K) { return N >= 1 && K >= kK && K % kK == 0; }
 
+// Token tile: the grid is (row-tile pairs) x (token tiles), one CTA per SM, so its time is set by the
+// rounds ceil(tiles / #SMs) of one tile each.  A tile costs about (tokens + 96) token-units (the 96:
+// epilogue and pipeline fill, fitted to the A/B below); pick the width (multiple of 32, >= 128) that
+// minimises rounds x cost, larger on ties.  Measured (tools/prefill_bench.py, K9 per device, forced
+// widths 256 / 224 / 192 / 160 / 128): 4K 518 / 478 / 527 / 503 / 638 µs, 1K 133 / 150 / 214 / 199 / 192;
+// the rule picks 224 for the W^O GEMM at 4K (448 tiles of 256 = 4 rounds for 3.03 of work -> 532 of
+// 224) and at 1K, 256 for the k / v up-projections.  TPLA_K9_TN forces one width (A/B).
+static int pick_tn(int n_rp, int L) {
+  static const int forced = getenv("TPLA_K9_TN") ? atoi(getenv("TPLA_K9_TN")) : 0;
+  if (forced >= 32 && forced <= kN && forced % 32 == 0) return forced;
+  const int sms = sm_count9();
+  int best = kN;
+  long best_cost = -1;
+  for (int tn = kN; tn >= 128; tn -= 32) {
+    const long tiles = long(n_rp) * ((L + tn - 1) / tn);
+    const long cost = (tiles + sms - 1) / sms * (tn + 96);
+    if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = tn; }
+  }
+  return best;
+}
+
 cudaError_t launch_gemm_tn(const uint16_t* Wt, const uint16_t* X, long ld_x, int N, int K, int L, float* y,
                            bool accumulate, uint16_t* out, cudaStream_t s) {
-  const int n_rt = (N + kM - 1) / kM, n_tt = (L + kN - 1) / kN, n_rp = (n_rt + kMT - 1) / kMT;
+  const int n_rt = (N + kM - 1) / kM, n_rp = (n_rt + kMT - 1) / kMT;
+  const int tn = pick_tn(n_rp, L), n_tt = (L + tn - 1) / tn;
   if (y && accumulate && out) return cudaErrorInvalidValue;   // (the bf16 copy of an accumulated y: not here)
   CUtensorMap mw, mx, my{}, mo{};
-  if (!map2d(&mw, Wt, kK, long(n_rt) * (K / kK) * kM, kK, kM) || !map2d(&mx, X, K, L, ld_x, kN))
+  if (!map2d(&mw, Wt, kK, long(n_rt) * (K / kK) * kM, kK, kM) || !map2d(&mx, X, K, L, ld_x, tn))
     return cudaErrorInvalidValue;
   if (y && !map2d(&my, y, N, L, N, 32, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
@@ -195,7 +230,7 @@ cudaError_t launch_gemm_tn(const uint16_t* Wt, const uint16_t* X, long ld_x, int
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  G9Args a{y, out, N, L, K / kK, n_tt, n_rt, accumulate ? 1 : 0};
+  G9Args a{y, out, N, L, K / kK, n_tt, n_rt, accumulate ? 1 : 0, tn};
   KernelScope ks("K9_prefill_gemm", s);
   return launch_k(gemm_tn_kernel, n_rp * n_tt, 384, kSmem, s, mw, mx, my, mo, a);
 }
