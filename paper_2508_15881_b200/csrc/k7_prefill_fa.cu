@@ -35,6 +35,13 @@
 namespace tpla {
 namespace {
 
+// Polynomial exp2 share of the softmax: iterations c (step 2) with (c & kPolyMask) == 0 compute two of
+// their four exponentials on the FMA pipe — 6: 1 in 8 (default), 2: 1 in 4, 0: 1 in 2, -1: none.
+#ifndef TPLA_K8_POLY_MASK
+#define TPLA_K8_POLY_MASK 6
+#endif
+constexpr int kPolyMask = TPLA_K8_POLY_MASK;
+
 using namespace sm100;
 
 constexpr int kT = 128;               // queries per CTA = keys per tile
@@ -264,7 +271,7 @@ attn_fwd_causal_kernel(const __grid_constant__ CUtensorMap mq, const __grid_cons
           f2_unpack(ffma2(f2_pack(x[2 * c + 2], x[2 * c + 3]), sc2, nm2), y2, y3);
           const float p0 = ex2(y0), p1 = ex2(y1);
           float p2, p3;
-          if ((c & 6) == 0) {
+          if (kPolyMask >= 0 && (c & kPolyMask) == 0) {
             ex2_poly2(y2, y3, p2, p3);               // 1 in 8 on the FMA pipe (arguments <= 8)
           } else {
             p2 = ex2(y2);

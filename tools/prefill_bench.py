@@ -145,11 +145,15 @@ def main():
     ap.add_argument("--L", type=int, nargs="+", default=[1024, 4096])
     ap.add_argument("--k", type=int, default=2)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--fwd-only", action="store_true", help="only the non-absorbed MLA forward (A/B runs)")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     rows = []
     for L in a.L:
         fwd = run_fwd(L, a.k, a.iters, dev)
+        if a.fwd_only:
+            print(json.dumps({"L": L, "mla_fwd": fwd}), flush=True)
+            continue
         mla = run(L, a.k, 1, a.iters, dev)
         tp = run(L, a.k, a.k, a.iters, dev)
         rows.append({"L": L, "mla_fwd": fwd, "mla_abs": mla, "tpla_abs": tp,
