@@ -140,7 +140,11 @@ struct Cfg {
   // per-CTA end times (h8, c1): at 512 tokens the two-segment CTAs ended 3-4 us after the others
   // (every one of the slowest eight had two segments).  A/B of the in-step K3 time over 512 / 768 /
   // 1024 / 1536 tokens: 1024 best at W_lat 64 / 256 (h8 -3.5 %, c1 -4 %, c3 -3 %), 512 at W_lat 128.
-  static constexpr int SEQ_COST = (TPLA_SEQ_COST_TOKENS > 0 ? TPLA_SEQ_COST_TOKENS : W_LAT == 128 ? 512 : 1024) / TT;
+  // Re-fitted at the end of round 2 (per-CTA end times of the trace against tiles and segment count:
+  // an extra segment costs ~6 tiles at h8 and ~6-8 at c1 once the partials are fp16) and A/B'd: 512
+  // tokens at W_lat 256 (c1 K3 243.5 -> 240.5 us per step), 768 at W_lat 64 (h8 476.3 -> 474.9).
+  static constexpr int SEQ_COST = (TPLA_SEQ_COST_TOKENS > 0 ? TPLA_SEQ_COST_TOKENS
+                                   : W_LAT == 128 || W_LAT == 256 ? 512 : W_LAT == 64 ? 768 : 1024) / TT;
   static constexpr int W = WL + 64;
   static constexpr int NBOX = W / 64;                 // 64-column groups per tile (latent part + RoPE)
   static constexpr int SUB_BYTES = kSub * 128;        // one TMA box: 64 rows x 128 B
