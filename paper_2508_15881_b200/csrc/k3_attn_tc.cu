@@ -355,6 +355,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   __shared__ uint32_t tmem_base;
   __shared__ int cum[kMaxB + 1];
   __shared__ int slen[kMaxB];            // min(seq_len, capacity) per sequence
+  __shared__ int s_rows[32];             // the first 32 box rows of the range (K3p)
   __shared__ int s_sched[5];             // this CTA's plan entry: lo, hi, b_first, b_last, seg_base
   __shared__ float red_max[C::NSB][2][128];   // [S buffer][half][row] partial row maxima
   __shared__ float red_l[2][128];        // [half][row] partial row sums at a segment end
@@ -384,12 +385,93 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   // sequence scan, the range starts and the first page-table lookups took ~10 K cycles per CTA
   // before the first TMA — measured, trace mode — with the SMs' HBM streams idle.)
   if (threadIdx.x == 0) EV(1);
+  // Softmax warps' row geometry (warps >= 4; harmless elsewhere).  Multi-token decode (n_q > 1,
+  // SURVEY f3): row r = (token i, head h).
+  const int q4 = warp & 3;
+  const int half = (warp - 4) >> 2;                     // 0 or 1 for the softmax warps
+  const int r = q4 * 32 + lane;                         // head row = TMEM lane
+  const int n_rows = a.n_q * a.h_loc;
+  const bool row_ok = r < n_rows;
+  const int tok_i = row_ok ? r / a.h_loc : 0, head_h = row_ok ? r % a.h_loc : 0;
+  // Q'_j row (bf16 pairs, this warp's columns) and the q^PE chunks 4*half .. 4*half+3 of sequence bb
+  // into registers; q_store (softmax branch) moves them to TMEM / smem.
+  constexpr int QC = C::WL / 2;                         // packed columns of Q'_j
+  constexpr int QH = QC / 2 >= 32 ? QC / 2 : 32;        // columns per warp (W_LAT=64: one warp does all)
+  const int q_cbegin = QC / 2 >= 32 ? half * QH : 0;
+  const bool q_loads = QC / 2 >= 32 || half == 0;
+  struct QRegs { uint4 pe[4]; uint4 q[QH / 4]; };
+  auto q_fetch = [&](int bb, QRegs& v) {
+    const uint4* pe = reinterpret_cast<const uint4*>(
+        a.q_pe + (((long)bb * a.n_q + tok_i) * a.h_q + a.head_begin + head_h) * 64);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v.pe[c] = row_ok ? pe[4 * half + c] : make_uint4(0, 0, 0, 0);
+    const uint4* src = reinterpret_cast<const uint4*>(
+        a.q_lat + (((long)bb * a.n_q + tok_i) * a.h_loc + head_h) * W_LAT + crank * C::WL);
+#pragma unroll
+    for (int v4 = 0; v4 < QH / 4; ++v4)
+      v.q[v4] = row_ok && q_loads ? src[q_cbegin / 4 + v4] : make_uint4(0, 0, 0, 0);
+  };
+  // One ring stage (tile g of the range): its TT/64 boxes per 64-column group, rows from the
+  // producer's batch of 32 resolved box rows.
+  auto issue_stage = [&](int g, int rows_batch) {
+    int row[C::SUB];
+#pragma unroll
+    for (int r = 0; r < C::SUB; ++r) row[r] = __shfl_sync(0xffffffffu, rows_batch, (g * C::SUB + r) & 31);
+    const int st = g % C::NST;
+    if (elect_one()) {
+      TRACE(14, g);
+      if (g == 0) EV(4);
+      uint8_t* dst = s_kv + st * C::STAGE_BYTES;
+      if (MODE & 4) {
+        mbar_arrive(&kv_full[st]);      // diagnostic: no HBM traffic, stale smem contents
+      } else {
+        mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
+#pragma unroll
+        for (int j = 0; j < C::NBOX; ++j)
+#pragma unroll
+          for (int r = 0; r < C::SUB; ++r)
+            tma_load_2d(dst + j * C::BOX_BYTES + r * C::SUB_BYTES, &tmap,
+                        j < C::NBOX - 1 ? int(crank) * C::WL + j * 64 : W_LAT, row[r], &kv_full[st], kEvictFirst);
+      }
+    }
+    __syncwarp();
+  };
   pdl_wait();          // the plan (K3p), Q' (K2) and the appended rows (K1) come from the predecessors
-  {
+  // Warp 3 (otherwise idle) fills the first ring stages straight after the wait: the range and the
+  // first 32 box rows (resolved by K3p) are read in one round trip, concurrently with the CTA's plan
+  // loads by the other warps (the producer, issuing after those, waited for a second dependent round
+  // trip: ~2400 cycles of an h8 CTA's ~6400-cycle start, trace mode).  The empty ring needs no
+  // kv_empty waits; the producer continues at stage n_early.
+  // The softmax warps fetch the first segment's Q'_j / q^PE (plan entry, then the rows) before that
+  // burst of cache loads reaches HBM (named barrier kQBar: queued behind it, the fetch took ~7 K
+  // cycles and became the start's critical path, trace mode).
+  static_assert(C::NST * C::SUB < 32, "the early stages come from the first batch of box rows");
+  constexpr uint32_t kQBar = 13;                        // 8 softmax warps + warp 3
+  QRegs q0;
+  bool q0_ok = false;
+  if (warp == 3) {
+    const int32_t* pl = a.plan;
+    const int rows_first = pl[n_cta * kPlanStride + 2 * a.B + 1 + c * 32 + lane];
+    const int lo0 = pl[c * kPlanStride], hi0 = pl[c * kPlanStride + 1];
+    const int n_early = max(0, min(C::NST, hi0 - lo0));
+    named_bar_sync(kQBar, 288);
+    if (lane == 0) EV(2);
+    for (int g = 0; g < n_early; ++g) issue_stage(g, rows_first);
+    s_rows[lane] = rows_first;                          // the producer's first batch (a reload would queue
+                                                        // behind the burst: ~8 K cycles, the ring drained)
+  } else if (warp >= 4) {
+    const int32_t* pl = a.plan;
+    const int b0 = pl[c * kPlanStride + 2], b1 = pl[c * kPlanStride + 3];
+    q0_ok = b0 <= b1;
+    if (q0_ok) q_fetch(b0, q0);
+    named_bar_arrive(kQBar, 288);
+  }
+  if (warp != 3) {
     const int32_t* pl = a.plan;
     const int off_cum = n_cta * kPlanStride, off_slen = off_cum + a.B + 1;
-    for (int i = tid; i <= a.B; i += kThreads) cum[i] = pl[off_cum + i];
-    for (int i = tid; i < a.B; i += kThreads) slen[i] = pl[off_slen + i];
+    const int i0 = tid < 96 ? tid : tid - 32;           // every thread but warp 3's
+    for (int i = i0; i <= a.B; i += kThreads - 32) cum[i] = pl[off_cum + i];
+    for (int i = i0; i < a.B; i += kThreads - 32) slen[i] = pl[off_slen + i];
     if (tid < 5) s_sched[tid] = pl[c * kPlanStride + tid];
   }
   tc_fence_before();
@@ -425,38 +507,18 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       if (tok >= slen[bb]) tok = tok0;
       return a.block_table[(long)bb * a.max_pages + tok / a.page_size] * a.page_size + tok % a.page_size;
     };
-    if (lane == 0) EV(2);
-    int rows_cur = a.plan[n_cta * kPlanStride + a.B + 1 + a.B + c * 32 + lane];   // K3p resolved the first 32
+    const int n_early = max(0, min(C::NST, S.hi - S.lo));   // stages warp 3 issued
+    int rows_cur = s_rows[lane];                       // K3p resolved the first 32 (warp 3 read them)
     int rows_next = lookup(32 + lane);                 // (in flight while the first batch streams)
     if (lane == 0) EV(3);
-    for (int t = S.lo, g = 0; t < S.hi; ++t, ++g) {
+    for (int t = S.lo + n_early, g = n_early; t < S.hi; ++t, ++g) {
       const int u0 = g * C::SUB;                       // SUB divides 32: a tile never spans batches
       if (u0 > 0 && (u0 & 31) == 0) {
         rows_cur = rows_next;
         rows_next = lookup(u0 + 32 + lane);
       }
-      int row[C::SUB];
-#pragma unroll
-      for (int r = 0; r < C::SUB; ++r) row[r] = __shfl_sync(0xffffffffu, rows_cur, (u0 + r) & 31);
-      const int st = g % C::NST;
-      mbar_wait(&kv_empty[st], ((g / C::NST) & 1) ^ 1);
-      if (elect_one()) {
-        TRACE(14, g);
-        if (g == 0) EV(4);
-        uint8_t* dst = s_kv + st * C::STAGE_BYTES;
-        if (MODE & 4) {
-          mbar_arrive(&kv_full[st]);      // diagnostic: no HBM traffic, stale smem contents
-        } else {
-          mbar_arrive_expect_tx(&kv_full[st], C::STAGE_BYTES);
-#pragma unroll
-          for (int j = 0; j < C::NBOX; ++j)
-#pragma unroll
-            for (int r = 0; r < C::SUB; ++r)
-              tma_load_2d(dst + j * C::BOX_BYTES + r * C::SUB_BYTES, &tmap,
-                          j < C::NBOX - 1 ? int(crank) * C::WL + j * 64 : W_LAT, row[r], &kv_full[st], kEvictFirst);
-        }
-      }
-      __syncwarp();
+      mbar_wait(&kv_empty[g % C::NST], ((g / C::NST) & 1) ^ 1);
+      issue_stage(g, rows_cur);
     }
   } else if (MODE == 1 && warp == 1) {
     int g = 0;
@@ -628,51 +690,32 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     // Two warps per TMEM lane quadrant: warp 4+q handles S columns [0,32) (tokens 0-31 of the
     // tile), warp 8+q columns [32,64), for the same 32 head rows; they exchange their partial
     // row maxima through shared memory so both take the same rescale decisions.
-    const int q4 = warp & 3;
-    const int half = (warp - 4) >> 2;                   // 0 or 1
-    const int r = q4 * 32 + lane;                       // head row = TMEM lane
     const uint32_t lane_base = tb + (uint32_t(q4 * 32) << 16);
-    // Multi-token decode (n_q > 1): row r = (token i, head h); token i of sequence b sits
-    // at position S_b - n_q + i and attends to the first S_b - n_q + 1 + i cached tokens (causal
-    // among the new tokens, which are already in the cache).
-    const int n_rows = a.n_q * a.h_loc;
-    const bool row_ok = r < n_rows;
+    // Multi-token decode: token i of sequence b sits at position S_b - n_q + i and attends to the
+    // first S_b - n_q + 1 + i cached tokens (causal among the new tokens, already in the cache).
     const bool q_active = q4 * 32 < n_rows;             // warp-uniform: this quadrant holds rows
-    const int tok_i = row_ok ? r / a.h_loc : 0, head_h = row_ok ? r % a.h_loc : 0;
     const int len_adj = tok_i + 1 - a.n_q;              // this row's visible length = S_b + len_adj
     const float sc = a.scale_log2;
     const uint32_t pair_bar = 1 + q4;                   // named barrier of the two warps of a quadrant
     // Q'_j row -> TMEM (A operand, bf16 pairs per 32-bit column), half of it per warp;
     // q^PE row -> swizzled smem (chunks 4*half .. 4*half+3); then signal the MMA warp
-    // (the q^PE loads are issued first: the Q' TMEM stores are asm volatile with a memory clobber,
-    // so loads placed after them would wait for a second round trip)
-    auto load_q = [&](int bb) {
-        const uint4* pe = reinterpret_cast<const uint4*>(
-            a.q_pe + (((long)bb * a.n_q + tok_i) * a.h_q + a.head_begin + head_h) * 64);
-        uint4 pev[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) pev[c] = row_ok ? pe[4 * half + c] : make_uint4(0, 0, 0, 0);
-        const uint4* src = reinterpret_cast<const uint4*>(
-            a.q_lat + (((long)bb * a.n_q + tok_i) * a.h_loc + head_h) * W_LAT + crank * C::WL);
-        constexpr int QC = C::WL / 2;                   // packed columns of Q'_j
-        constexpr int QH = QC / 2 >= 32 ? QC / 2 : 32;  // columns per warp (W_LAT=64: one warp does all)
-        const int c_begin = QC / 2 >= 32 ? half * QH : 0;
-        if (QC / 2 >= 32 || half == 0) {
+    auto q_store = [&](const QRegs& v, int bb) {
+        if (q_loads) {
 #pragma unroll
           for (int c0 = 0; c0 < QH; c0 += 32) {
             uint32_t w[32];
 #pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              uint4 u = row_ok ? src[(c_begin + c0) / 4 + v] : make_uint4(0, 0, 0, 0);
-              w[4 * v] = u.x; w[4 * v + 1] = u.y; w[4 * v + 2] = u.z; w[4 * v + 3] = u.w;
+            for (int k = 0; k < 8; ++k) {
+              const uint4 u = v.q[c0 / 4 + k];
+              w[4 * k] = u.x; w[4 * k + 1] = u.y; w[4 * k + 2] = u.z; w[4 * k + 3] = u.w;
             }
-            tmem_st32(lane_base + C::Q_COL + c_begin + c0, w);
+            tmem_st32(lane_base + C::Q_COL + q_cbegin + c0, w);
           }
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int ch = 4 * half + c;
-          *reinterpret_cast<uint4*>(s_qpe + r * 128 + ((ch ^ (r & 7)) << 4)) = pev[c];
+          *reinterpret_cast<uint4*>(s_qpe + r * 128 + ((ch ^ (r & 7)) << 4)) = v.pe[c];
         }
         fence_proxy_async_smem();
         tmem_st_wait();
@@ -680,6 +723,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&q_ready);
         if (warp == 4 && lane == 0 && bb == S.b_first) EV(5);
+    };
+    // (the loads are all issued before the Q' TMEM stores, which are asm volatile with a memory
+    // clobber: loads placed after them would wait for a second round trip)
+    auto load_q = [&](int bb) {
+        QRegs v;
+        q_fetch(bb, v);
+        q_store(v, bb);
     };
     if constexpr (C::PP) {
     // ---- ping-pong softmax (TT = 128).  Warp set `half` takes the tiles with g % 2 == half, whole
@@ -730,7 +780,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
       return (a0 + a1) + (a2 + a3);
     };
     int g = 0, seg = 0;
-    if (S.b_first <= S.b_last) load_q(S.b_first);
+    if (q0_ok) q_store(q0, S.b_first);               // fetched in the prologue
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
       const int S_b = slen[b] + len_adj;                 // this row's visible length
@@ -869,7 +919,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
     } else {
     int g = 0, seg = 0;
     int xk = 0;                                          // PAIR: logit exchanges done by this warp
-    if (S.b_first <= S.b_last) load_q(S.b_first);
+    if (q0_ok) q_store(q0, S.b_first);               // fetched in the prologue
     for (int b = S.b_first; b <= S.b_last; ++b, ++seg) {
       const int t0 = max(S.lo, cum[b]), t1 = min(S.hi, cum[b + 1]);
       const int S_b = slen[b] + len_adj;                 // this row's visible length
@@ -1075,6 +1125,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a) {
   if ((MODE & 2) && tid == 0) {
     a.trace[kSlots * kTrace + 2 * c + 1] = globaltimer();
     a.trace[kSlots * kTrace + 2 * kMaxCta + 2 * c + 1] = clock64();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    long long* ci = a.trace + kSlots * kTrace + 4 * kMaxCta + 16;   // per-CTA (smid, tiles, segments)
+    ci[3 * c] = smid;
+    ci[3 * c + 1] = S.hi - S.lo;
+    ci[3 * c + 2] = S.b_last - S.b_first + 1;
   }
   if (C::PAIR) cluster_sync();   // the peer may still be writing into our smem / arriving on our barriers
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tb);
@@ -1172,7 +1228,7 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
   if (mode && strncmp(mode, "trace", 5) == 0) {   // trace, trace_notma, trace_nold
     static long long* buf = nullptr;
     const int nb = kSlots * kTrace + 2 * n_cta;
-    if (!buf) cudaMalloc(&buf, (kSlots * kTrace + 4 * kMaxCta + 16) * sizeof(long long));
+    if (!buf) cudaMalloc(&buf, (kSlots * kTrace + 7 * kMaxCta + 16) * sizeof(long long));
     TcArgs b = a;
     b.trace = buf;
     const char* tc = getenv("TPLA_K3_TRACE_CTA");
@@ -1181,9 +1237,9 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
                     : strcmp(mode, "trace_nosm") == 0  ? launch_tc_mode<W_LAT, 2 | 4 | 16>(map, b, n_cta, s)
                     : strcmp(mode, "trace_nold") == 0  ? launch_tc_mode<W_LAT, 10>(map, b, n_cta, s)
                                                         : launch_tc_mode<W_LAT, 2>(map, b, n_cta, s);
-    static long long h[kSlots * kTrace + 4 * kMaxCta + 16];
+    static long long h[kSlots * kTrace + 7 * kMaxCta + 16];
     cudaStreamSynchronize(s);
-    cudaMemcpy(h, buf, (kSlots * kTrace + 4 * kMaxCta + 16) * sizeof(long long), cudaMemcpyDeviceToHost);
+    cudaMemcpy(h, buf, (kSlots * kTrace + 7 * kMaxCta + 16) * sizeof(long long), cudaMemcpyDeviceToHost);
     (void)nb;
     const long long* cs = h + kSlots * kTrace;
     const long long* cc = cs + 2 * kMaxCta;        // clock64 at the same two points
@@ -1203,6 +1259,13 @@ cudaError_t launch_tc(const CUtensorMap& map, const TcArgs& a, int n_cta, cudaSt
     fprintf(stderr, "[k3 ends]");                   // every CTA's end (ns), for balance analysis
     for (int c = 0; c < n_cta; ++c) fprintf(stderr, " %lld", cs[2 * c + 1] - t0);
     fprintf(stderr, "\n");
+    {
+      const long long* ci = h + kSlots * kTrace + 4 * kMaxCta + 16;
+      fprintf(stderr, "[k3 ctainfo] cta smid tiles segs start_ns end_ns\n");
+      for (int c = 0; c < n_cta; ++c)
+        fprintf(stderr, "[k3 ctainfo] %d %lld %lld %lld %lld %lld\n", c, ci[3 * c], ci[3 * c + 1], ci[3 * c + 2],
+                cs[2 * c] - t0, cs[2 * c + 1] - t0);
+    }
     fprintf(stderr, "[k3 cta] traced CTA: start -> qk_issue[0] %lld cycles, qk_issue[0] -> end %lld cycles\n",
             h[0] - cc[2 * b.trace_cta], cc[2 * b.trace_cta + 1] - h[0]);
     {
