@@ -42,10 +42,20 @@ __global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
 
   // W^UV'_j[h] -> smem (does not depend on the predecessor: issue before the PDL wait)
   const uint16_t* wsrc = a.W_UV + (long)h * a.d_h * a.w_lat;
-  const int chunks = a.d_h * (a.w_lat / 8);
-  for (int c = tid; c < chunks; c += kThreads) {
-    const int r = c / (a.w_lat / 8), ch = c % (a.w_lat / 8);
-    cp_async16(sW + r * WP + ch * 8, wsrc + (long)r * a.w_lat + ch * 8, true);
+  // (16-byte chunks per weight row: a power of two for every W_lat = d_c / g, so shifts instead of
+  // integer divisions — the division loop had been ~30 % of the kernel's instructions, ncu source)
+  const int cpr = a.w_lat / 8, chunks = a.d_h * cpr;
+  if ((cpr & (cpr - 1)) == 0) {
+    const int sh = __ffs(cpr) - 1;
+    for (int c = tid; c < chunks; c += kThreads) {
+      const int r = c >> sh, ch = c & (cpr - 1);
+      cp_async16(sW + r * WP + ch * 8, wsrc + (long)r * a.w_lat + ch * 8, true);
+    }
+  } else {
+    for (int c = tid; c < chunks; c += kThreads) {
+      const int r = c / cpr, ch = c % cpr;
+      cp_async16(sW + r * WP + ch * 8, wsrc + (long)r * a.w_lat + ch * 8, true);
+    }
   }
   cp_async_commit();
   pdl_wait();
@@ -198,7 +208,8 @@ __global__ void __launch_bounds__(kThreads, 2) combine_wuv_kernel(FArgs a) {
         if (b < a.B * a.n_q) {
           if (a.v_acc) {                            // (each element has exactly one writer: no atomics)
             const int kc = a.h_loc * a.d_h / a.v_chunks, c = h * a.d_h + e;   // (kc even: e, c even)
-            const long idx = (long(c / kc) * a.B * a.n_q + b) * kc + c % kc;
+            const int cq = (kc & (kc - 1)) == 0 ? c >> (__ffs(kc) - 1) : c / kc;
+            const long idx = (long(cq) * a.B * a.n_q + b) * kc + (c - cq * kc);
             float2 o = make_float2(acc[2 * hh], acc[2 * hh + 1]);
             if (a.v_acc_add) {
               const float2 p = *reinterpret_cast<const float2*>(a.v_acc + idx);
